@@ -1,0 +1,915 @@
+// nrldpc: B200-native layered min-sum LDPC decoder (sm_100a) + C ABI.
+//
+// Hot path replaced: ldpclab.decoder.decode / _run_schedule / layered_iteration
+// / _scalar_layer (/root/reference/pkg/src/ldpclab/decoder.py:295-320,
+// 459-469, 486-566) and ldpclab.channel.quantize (channel.py:64-83).
+// See DESIGN.md for the layout and roofline; nrldpc_kernels.cuh for the exact
+// half2 arithmetic argument.
+
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "nrldpc_kernels.cuh"
+#include "../../include/nrldpc.h"
+
+using namespace nr;
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local int g_launches = 0;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  return NRLDPC_ECUDA;
+}
+
+#define NR_CUDA(call)                                    \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);  \
+  } while (0)
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Device code
+
+namespace nr {
+
+struct GroupState {
+  int synd[2];
+  int minabs[2];
+  int done[2];
+  int accept[2];
+};
+
+struct CtaState {
+  int n_done;
+  int n_valid;
+  int pad[2];
+};
+
+constexpr int kLutBytes = 256;
+constexpr int kCtaBytes = 16;
+
+// (z + s) mod Z for one edge, as a byte offset into the group's L array.
+__device__ __forceinline__ uint32_t edge_offset(const KParams& p, int e, uint32_t zl, uint32_t ZL) {
+  uint32_t a = zl + p.shift_l[e];
+  a = min(a, a - ZL);  // unsigned: picks a-ZL only when a >= ZL  (one VIADDMNMX)
+  return a + p.colbase[e];
+}
+
+// One layer (base row r) for thread (group, z): gather, min-sum check-node
+// update, scatter. decoder.py:295-320. Messages are thread-major
+// (Mz = this thread's message row), so edge j of the row is at Mrow + j*LANES.
+template <int MAXW, int LANES>
+__device__ __forceinline__ void process_row(const KParams& p, const int e0, const int w, uint32_t zl,
+                                            uint32_t ZL, uint8_t* __restrict__ Lg,
+                                            uint8_t* __restrict__ Mz, const uint16_t* __restrict__ lut,
+                                            uint32_t magic, uint32_t one, bool st_ok) {
+  const half2 H127 = u2h(0x57F057F0u);   // 127.0
+  const half2 H1152 = u2h(0x64806480u);  // 1152.0
+  uint8_t* Mrow = Mz + e0 * LANES;
+  uint32_t off[MAXW];
+  half2 t[MAXW];
+  half2 m1 = H127, m2 = H127;
+  uint32_t S = 0;
+#pragma unroll
+  for (int j = 0; j < MAXW; ++j) {
+    if (j < w) {
+      off[j] = edge_offset(p, e0 + j, zl, ZL);
+      const half2 lh = unpack_elem<LANES>(ld_elem<LANES>(Lg + off[j]), magic);
+      const half2 mh = unpack_elem<LANES>(ld_elem<LANES>(Mrow + j * LANES), magic);
+      const half2 tj = __hsub2(lh, mh);           // exact: L - M
+      const half2 aj = __habs2(tj);
+      m2 = __hmin2(m2, __hmax2(m1, aj));          // kernels.py:247-250
+      m1 = __hmin2(m1, aj);
+      S ^= h2u(tj);                               // sign product (bits 15/31)
+      t[j] = tj;
+    }
+  }
+  // beta-scaled magnitudes, with the row sign folded in: b' = (-1)^S * b
+  const half2 b1 = beta_lut2(lut, m1);
+  const half2 b2 = beta_lut2(lut, m2);
+  const half2 sig = u2h((S & 0x80008000u) | one);
+  const half2 d = __hmul2(__hsub2(b2, b1), sig);
+  const half2 b1s = __hmul2(b1, sig);
+#pragma unroll
+  for (int j = 0; j < MAXW; ++j) {
+    if (j < w) {
+      const half2 aj = __habs2(t[j]);
+      // edge holding the minimum gets m2 (a tie implies m1 == m2)
+      const half2 mag = __hfma2(__heq2(aj, m1), d, b1s);
+      // L' = sign(t) * min(|clamp t| + mag', 127)   == clamp127(t + out)
+      const half2 y = __hmin2(__hadd2(__hmin2(aj, H127), mag), H127);
+      const half2 sg = u2h((h2u(t[j]) & 0x80008000u) | one);
+      st_elem_if<LANES>(Lg + off[j], pack_elem<LANES>(__hfma2(y, sg, H1152)), st_ok);
+      st_elem_if<LANES>(Mrow + j * LANES, pack_elem<LANES>(__hfma2(mag, sg, H1152)), st_ok);
+    }
+  }
+}
+
+// Syndrome weight (decoder.py:323-329) and min|L| (decoder.py:480-483) over
+// the thread's check rows / columns.
+template <int MAXW, int LANES>
+__device__ __forceinline__ void row_parity(const KParams& p, const int e0, const int w, uint32_t zl,
+                                           uint32_t ZL, const uint8_t* __restrict__ Lg, int& wa,
+                                           int& wb) {
+  uint32_t x = 0;
+#pragma unroll
+  for (int j = 0; j < MAXW; ++j) {
+    if (j < w) x ^= ld_elem<LANES>(Lg + edge_offset(p, e0 + j, zl, ZL));
+  }
+  // bit 7 of a stored byte is 1 for a non-negative value
+  if (w & 1) x ^= 0x8080u;
+  wa += (x >> 7) & 1u;
+  wb += (x >> 15) & 1u;
+}
+
+// Layer schedules. Generic: row tables read at run time. BG1/BG2: the row
+// weights are compile-time (they are fixed by the base graph), so every
+// edge's shift/column becomes a constant-bank operand and the 46 (42)
+// layers are straight-line code with one uniform early-out on rows_used.
+template <int BG>
+struct RowW;
+template <>
+struct RowW<1> {
+  static constexpr int n = 46;
+  static constexpr int w[46] = {19, 19, 19, 19, 3, 8, 9, 7, 10, 9, 7, 8, 7, 6, 7, 7, 6, 6, 6, 6, 6, 6, 5,
+                                5,  6,  5,  5,  4, 5, 5, 5, 5,  5, 5, 5, 5, 5, 4, 5, 5, 4, 5, 4, 5, 5, 4};
+  static constexpr int e0[47] = {0, 19, 38, 57, 76, 79, 87, 96, 103, 113, 122, 129, 137, 144, 150, 157, 164, 170, 176, 182, 188, 194, 200, 205, 210, 216, 221, 226, 230, 235, 240, 245, 250, 255, 260, 265, 270, 275, 279, 284, 289, 293, 298, 302, 307, 312, 316};
+};
+template <>
+struct RowW<2> {
+  static constexpr int n = 42;
+  static constexpr int w[42] = {8, 10, 8, 10, 4, 6, 6, 6, 4, 5, 5, 5, 4, 5, 5, 4, 5, 5, 4, 4, 4,
+                                4, 3,  4, 4,  3, 5, 3, 4, 3, 5, 3, 4, 4, 4, 4, 4, 3, 4, 4, 4, 4};
+  static constexpr int e0[43] = {0, 8, 18, 26, 36, 40, 46, 52, 58, 62, 67, 72, 77, 81, 86, 91, 95, 100, 105, 109, 113, 117, 121, 124, 128, 132, 135, 140, 143, 147, 150, 155, 158, 162, 166, 170, 174, 178, 181, 185, 189, 193, 197};
+};
+
+struct RowCtx {
+  uint32_t zl, ZL;
+  uint8_t* Lg;
+  uint8_t* Mz;
+  const uint16_t* lut;
+  uint32_t magic, one;
+  bool st_ok;
+};
+
+template <int BG, int MAXW, int LANES, int R>
+__device__ __forceinline__ void layers_ct(const KParams& p, const RowCtx& c) {
+  if constexpr (R < RowW<BG>::n) {
+    if (R < p.rows) {
+      constexpr int E0 = RowW<BG>::e0[R];
+      constexpr int W = RowW<BG>::w[R];
+      process_row<MAXW, LANES>(p, E0, W, c.zl, c.ZL, c.Lg, c.Mz, c.lut, c.magic,
+                               c.one, c.st_ok);
+      __syncthreads();
+      layers_ct<BG, MAXW, LANES, R + 1>(p, c);
+    }
+  }
+}
+
+template <int BG, int MAXW, int LANES, int R>
+__device__ __forceinline__ void parity_ct(const KParams& p, uint32_t zl, uint32_t ZL,
+                                          const uint8_t* __restrict__ Lg, int& wa, int& wb) {
+  if constexpr (R < RowW<BG>::n) {
+    if (R < p.rows) {
+      constexpr int E0 = RowW<BG>::e0[R];
+      constexpr int W = RowW<BG>::w[R];
+      row_parity<MAXW, LANES>(p, E0, W, zl, ZL, Lg, wa, wb);
+      parity_ct<BG, MAXW, LANES, R + 1>(p, zl, ZL, Lg, wa, wb);
+    }
+  }
+}
+
+template <int BG, int MAXW, int LANES>
+__device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c) {
+  if constexpr (BG == 0) {
+    for (int r = 0; r < p.rows; ++r) {
+      const int e0 = p.row_start[r];
+      process_row<MAXW, LANES>(p, e0, p.row_start[r + 1] - e0, c.zl, c.ZL, c.Lg, c.Mz, c.lut, c.magic,
+                               c.one, c.st_ok);
+      __syncthreads();
+    }
+  } else {
+    layers_ct<BG, MAXW, LANES, 0>(p, c);
+  }
+}
+
+template <int BG, int MAXW, int LANES>
+__device__ __forceinline__ void local_check(const KParams& p, uint32_t zl, uint32_t ZL,
+                                            const uint8_t* __restrict__ Lg, int* wcnt, int* mabs) {
+  int wa = 0, wb = 0;
+  if constexpr (BG == 0) {
+    for (int r = 0; r < p.rows; ++r) {
+      const int e0 = p.row_start[r];
+      row_parity<MAXW, LANES>(p, e0, p.row_start[r + 1] - e0, zl, ZL, Lg, wa, wb);
+    }
+  } else {
+    parity_ct<BG, MAXW, LANES, 0>(p, zl, ZL, Lg, wa, wb);
+  }
+  int ma = 255, mb = 255;
+  for (int c = 0; c < p.n_blocks; ++c) {
+    const uint32_t u = ld_elem<LANES>(Lg + (uint32_t)c * ZL + zl);
+    ma = min(ma, abs((int)(u & 0xFFu) - 128));
+    mb = min(mb, abs((int)((u >> 8) & 0xFFu) - 128));
+  }
+  wcnt[0] = wa;
+  wcnt[1] = wb;
+  mabs[0] = ma;
+  mabs[1] = mb;
+}
+
+// Hard decisions of the first K positions, bit-packed LSB-first
+// (decoder.py:332-334).
+template <int LANES>
+__device__ __forceinline__ void write_bits(const KParams& p, const uint8_t* __restrict__ Lg, int z,
+                                           int lane, long long cw, uint32_t* __restrict__ bits) {
+  const int K = p.k_b * p.z;
+  for (int wi = z; wi < p.words; wi += p.z) {
+    const int base = wi * 32;
+    const int nb = min(32, K - base);
+    uint32_t word = 0;
+    for (int i = 0; i < nb; ++i) {
+      const uint32_t u = Lg[(base + i) * LANES + lane];
+      word |= (u < 128u ? 1u : 0u) << i;
+    }
+    bits[cw * p.words + wi] = word;
+  }
+}
+
+// Bit-serial CRC over the K hard bits (codec.py:183-213); true when the
+// register drains to zero.
+template <int LANES>
+__device__ bool crc_ok_serial(const KParams& p, const uint8_t* __restrict__ Lg, int lane) {
+  const int K = p.k_b * p.z;
+  if (K < p.crc_len) return false;
+  const uint32_t top = 1u << (p.crc_len - 1);
+  const uint32_t mask = (p.crc_len == 32) ? 0xFFFFFFFFu : ((1u << p.crc_len) - 1u);
+  uint32_t reg = 0;
+  for (int i = 0; i < K; ++i) {
+    const uint32_t bit = Lg[i * LANES + lane] < 128u ? 1u : 0u;
+    const uint32_t fb = ((reg & top) ? 1u : 0u) ^ bit;
+    reg = ((reg << 1) & mask) ^ (fb ? p.crc_poly : 0u);
+  }
+  return reg == 0;
+}
+
+// Layered decode of G groups x LANES codewords per CTA, everything resident
+// in shared memory for the whole decode (decoder.py:486-540).
+// Threads beyond G*Z (warp padding) shadow the last group's z = tid - (G-1)*Z
+// clamp but never store, so the layer loop runs warp-uniform and the graph
+// tables stay in uniform registers.
+template <int BG, int MAXW, int LANES>
+__global__ void __launch_bounds__(512) k_decode_i8(const __grid_constant__ KParams p,
+                                                   const int8_t* __restrict__ llr, KOut o) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint16_t* lut = reinterpret_cast<uint16_t*>(smem);
+  CtaState* cta = reinterpret_cast<CtaState*>(smem + kLutBytes);
+  GroupState* gstate = reinterpret_cast<GroupState*>(smem + kLutBytes + kCtaBytes);
+  const uint32_t data_off = (kLutBytes + kCtaBytes + (uint32_t)sizeof(GroupState) * p.groups + 15u) & ~15u;
+
+  const int tid = threadIdx.x;
+  const bool st_ok = tid < p.groups * p.z;           // not a padding thread
+  const int g = st_ok ? tid / p.z : p.groups - 1;
+  const int z = st_ok ? tid - g * p.z : (tid - g * p.z) % p.z;
+  const long long cw0 = ((long long)blockIdx.x * p.groups + g) * LANES;
+  const bool active = st_ok && cw0 < p.batch;        // owns real codewords
+  const uint32_t ZL = (uint32_t)p.z * LANES;
+  const uint32_t zl = (uint32_t)z * LANES;
+  const long long n_c = (long long)p.n_blocks * p.z;
+  uint8_t* Lg = smem + data_off + (uint32_t)g * (p.l_bytes + p.m_bytes);
+  uint8_t* Mz = Lg + p.l_bytes + (uint32_t)z * p.m_stride;
+  GroupState& gs = gstate[g];
+
+  for (int i = tid; i < 128; i += blockDim.x) lut[i] = p.lut[i];
+  if (tid == 0) {
+    const long long first = (long long)blockIdx.x * p.groups * LANES;
+    const long long rem = p.batch - first;
+    cta->n_done = 0;
+    cta->n_valid = (int)min(rem, (long long)p.groups * LANES);
+  }
+  if (st_ok && z == 0) {
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+      gs.synd[l] = 0;
+      gs.minabs[l] = 255;
+      gs.done[l] = 0;
+      gs.accept[l] = 0;
+    }
+  }
+
+  bool lane_valid[2];
+  lane_valid[0] = active;
+  lane_valid[1] = active && LANES == 2 && cw0 + 1 < p.batch;
+
+  // load: int8 -> biased byte (x ^ 0x80), lanes interleaved; messages = 0
+  if (st_ok) {
+    int bad = 0;
+    for (int c = 0; c < p.n_blocks; ++c) {
+      const long long n = (long long)c * p.z + z;
+      uint32_t v = 0;
+#pragma unroll
+      for (int l = 0; l < LANES; ++l) {
+        uint32_t u = 0x80u;
+        if (lane_valid[l]) {
+          const int8_t x = llr[(cw0 + l) * n_c + n];
+          bad |= (x == -128);
+          u = (uint32_t)(uint8_t)x ^ 0x80u;
+        }
+        v |= u << (8 * l);
+      }
+      st_elem<LANES>(Lg + (uint32_t)n * LANES, v);
+    }
+    for (int e = 0; e < p.n_edges; ++e) st_elem<LANES>(Mz + e * LANES, 0x8080u);
+    if (bad && o.status) atomicOr(o.status, 1);
+  }
+  __syncthreads();
+
+  const uint32_t magic = p.magic;  // 0x64646464, opaque to ptxas
+  const uint32_t one = p.one;      // 0x3C003C00 (half2 1.0)
+  const RowCtx rc{zl, ZL, Lg, Mz, lut, magic, one, st_ok};
+  for (int it = 1; it <= p.max_iter; ++it) {
+    one_iteration<BG, MAXW, LANES>(p, rc);
+    const bool last = it == p.max_iter;
+    if (!(p.early_stop != NRLDPC_STOP_NONE || p.trace || last)) continue;
+
+    // ---- end-of-iteration check (decoder.py:497-536) ----
+    {
+      int wc[2], ma[2];
+      local_check<BG, MAXW, LANES>(p, zl, ZL, Lg, wc, ma);
+      if (active) {
+#pragma unroll
+        for (int l = 0; l < LANES; ++l) {
+          if (wc[l]) atomicAdd(&gs.synd[l], wc[l]);
+          atomicMin(&gs.minabs[l], ma[l]);
+        }
+      }
+    }
+    __syncthreads();
+    int cand[2] = {0, 0};
+    if (active && p.early_stop != NRLDPC_STOP_NONE) {
+#pragma unroll
+      for (int l = 0; l < LANES; ++l)
+        cand[l] = lane_valid[l] && !gs.done[l] && gs.synd[l] == 0 && gs.minabs[l] > 0;
+    }
+    if (p.early_stop == NRLDPC_STOP_CRC) {
+      if (active && z == 0) {
+#pragma unroll
+        for (int l = 0; l < LANES; ++l) gs.accept[l] = cand[l] ? (int)crc_ok_serial<LANES>(p, Lg, l) : 0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int l = 0; l < LANES; ++l) cand[l] = cand[l] && gs.accept[l];
+    }
+    int fin[2] = {0, 0};  // not frozen at the last iteration: final values
+    if (active && last) {
+#pragma unroll
+      for (int l = 0; l < LANES; ++l) fin[l] = lane_valid[l] && !gs.done[l] && !cand[l];
+    }
+    if (active) {
+#pragma unroll
+      for (int l = 0; l < LANES; ++l) {
+        if (cand[l] || fin[l]) write_bits<LANES>(p, Lg, z, l, cw0 + l, o.bits);
+      }
+      if (z == 0) {
+#pragma unroll
+        for (int l = 0; l < LANES; ++l) {
+          if (!lane_valid[l]) continue;
+          const long long cw = cw0 + l;
+          const int wgt = gs.synd[l];
+          const int mar = gs.minabs[l];
+          if (p.trace) {
+            o.trace_w[cw * p.max_iter + (it - 1)] = wgt;
+            o.trace_m[cw * p.max_iter + (it - 1)] = (float)mar;
+          }
+          if (cand[l]) {
+            o.iters[cw] = it;
+            o.synd[cw] = 0;
+            o.success[cw] = 1;
+            if (o.crc_ok) o.crc_ok[cw] = 1;
+          } else if (fin[l]) {
+            o.iters[cw] = p.max_iter;
+            o.synd[cw] = wgt;
+            o.success[cw] = (p.early_stop == NRLDPC_STOP_NONE && wgt == 0 && mar > 0) ? 1 : 0;
+            if (o.crc_ok) o.crc_ok[cw] = 0;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (active && z == 0) {
+      int newly = 0;
+#pragma unroll
+      for (int l = 0; l < LANES; ++l) {
+        if (cand[l]) {
+          gs.done[l] = 1;
+          ++newly;
+        }
+        gs.synd[l] = 0;
+        gs.minabs[l] = 255;
+      }
+      if (newly) atomicAdd(&cta->n_done, newly);
+    }
+    __syncthreads();
+    // block-wide vote: provably uniform, so the layer loop stays on the
+    // uniform datapath (graph tables in uniform registers)
+    if (__syncthreads_and(!p.trace && cta->n_done >= cta->n_valid)) break;
+  }
+}
+
+// ---- quantize: depuncture + channel-domain -> decoder-domain LLRs ---------
+// channel.py:64-83; arithmetic in float64 like the reference.
+template <typename Tin, int MODE>
+__global__ void __launch_bounds__(256) k_quantize(const Tin* __restrict__ in, long long batch, int n_tx,
+                                                  int n_c, int two_z, double scale, double clip,
+                                                  void* __restrict__ out) {
+  const long long total = batch * (long long)n_c;
+  const long long stride = (long long)gridDim.x * blockDim.x * 4;
+  for (long long i0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4; i0 < total; i0 += stride) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const long long i = i0 + k;
+      if (i >= total) break;
+      const long long b = i / n_c;
+      const int j = (int)(i - b * n_c);
+      const double v = j < two_z ? 0.0 : (double)in[b * n_tx + (j - two_z)];
+      if (MODE == NRLDPC_INT8) {
+        double s = rint(v * scale);
+        s = fmin(fmax(s, -127.0), 127.0);
+        reinterpret_cast<int8_t*>(out)[i] = (int8_t)s;
+      } else if (MODE == NRLDPC_F16) {
+        double c = fmin(fmax(v, -clip), clip);
+        c = fmin(fmax(c, -65504.0), 65504.0);
+        reinterpret_cast<__half*>(out)[i] = __double2half(c);
+      } else {
+        const double c = fmin(fmax(v, -clip), clip);
+        reinterpret_cast<float*>(out)[i] = __double2float_rn(c);
+      }
+    }
+  }
+}
+
+// ---- ALU roofline microbenchmark -----------------------------------------
+// Eight independent half2 chains per thread; MIXED interleaves HMNMX2 (ALU
+// pipe) with HFMA2 (FMA pipe) 1:1 to find the dual-issue ceiling, otherwise
+// HMNMX2 only (ALU-pipe ceiling). Same instruction classes as the decode.
+template <bool MIXED>
+__global__ void __launch_bounds__(512) k_alu_peak(uint32_t* out, int iters, uint32_t seed) {
+  half2 a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = u2h(seed + threadIdx.x * 7919u + i * 104729u);
+  const half2 c = u2h(seed ^ 0x3C003C00u);
+  const half2 d = u2h(seed ^ 0x57F057F0u);
+  for (int k = 0; k < iters; ++k) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      a[i] = __hmin2(a[i], __habs2(d));
+      if (MIXED) a[i] = __hfma2(a[i], c, d);
+      else a[i] = __hmax2(a[i], c);
+    }
+  }
+  uint32_t x = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x ^= h2u(a[i]);
+  if (x == 0x12345678u) out[0] = x;  // keep the chains alive
+}
+
+}  // namespace nr
+
+// ---------------------------------------------------------------------------
+// Host side
+
+struct nrldpc_plan {
+  int device = 0;
+  int precision = NRLDPC_INT8;
+  int early_stop = NRLDPC_STOP_SYNDROME;
+  int crc_kind = NRLDPC_CRC24B;
+  double beta = 0.75;
+  int max_iter = 20;
+  int k_b = 0, z = 0, rows = 0, n_blocks = 0, n_edges = 0, maxw = 0;
+  int lanes = 1, groups = 1, threads = 32;
+  int schedule = 0;  // 0 generic, 1/2: compile-time BG1/BG2 row schedule
+  size_t smem = 0;
+  KParams kp{};
+  // host-path staging (nrldpc_decode_host)
+  std::mutex host_mu;
+  cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
+  void* d_buf = nullptr;
+  size_t d_cap = 0;
+};
+
+namespace {
+
+size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+// Per-thread message rows are padded so the row stride is an odd number of
+// 32-bit words: 32 consecutive z then hit 32 distinct banks.
+size_t padded_edges(int n_edges, int lanes) {
+  const size_t unit = lanes == 2 ? 2 : 4;  // stride bytes = e_pad*lanes = 4*(odd)
+  size_t e = (size_t)n_edges;
+  while (((e * lanes) % 4) != 0 || (((e * lanes) / 4) % 2) == 0) ++e;
+  (void)unit;
+  return e;
+}
+
+size_t smem_for(int groups, size_t l_bytes, size_t m_bytes) {
+  return kLutBytes + kCtaBytes + sizeof(GroupState) * groups + 16 + groups * (l_bytes + m_bytes);
+}
+
+template <int BG, int MAXW, int LANES>
+cudaError_t launch_i8(const nrldpc_plan* plan, const int8_t* llr, long long batch, const KOut& o,
+                      cudaStream_t st) {
+  static bool attr_done[64] = {};
+  const int dev = plan->device;
+  auto kern = k_decode_i8<BG, MAXW, LANES>;
+  if (!attr_done[dev & 63]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    if (e != cudaSuccess) return e;
+    attr_done[dev & 63] = true;
+  }
+  KParams kp = plan->kp;
+  kp.batch = batch;
+  kp.trace = o.trace_w != nullptr;
+  const long long per_cta = (long long)plan->groups * LANES;
+  const long long grid = (batch + per_cta - 1) / per_cta;
+  kern<<<(unsigned)grid, plan->threads, plan->smem, st>>>(kp, llr, o);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+int crc_params(int kind, int* len, uint32_t* poly) {
+  switch (kind) {
+    case NRLDPC_CRC24A: *len = 24; *poly = 0x864CFB; return 0;
+    case NRLDPC_CRC24B: *len = 24; *poly = 0x800063; return 0;
+    case NRLDPC_CRC16: *len = 16; *poly = 0x1021; return 0;
+    default: return -1;
+  }
+}
+
+uint16_t float_to_half_bits(float f) {
+  __half h = __float2half_rn(f);
+  uint16_t b;
+  std::memcpy(&b, &h, 2);
+  return b;
+}
+
+// Pick lanes (codewords per half2) and groups per CTA. Smaller CTAs keep the
+// per-layer barrier cheap; more codewords per SM come from more CTAs.
+void choose_shape(nrldpc_plan* p) {
+  const size_t smem_max = 232448;
+  const size_t n_pos = (size_t)p->n_blocks * p->z;
+  int lanes = 2;
+  if (smem_for(1, align16(n_pos * 2), align16((size_t)p->z * padded_edges(p->n_edges, 2) * 2)) > smem_max)
+    lanes = 1;
+  const size_t lb = align16(n_pos * lanes);
+  const size_t e_pad = padded_edges(p->n_edges, lanes);
+  const size_t mb = align16((size_t)p->z * e_pad * lanes);
+  int best_g = 1;
+  double best_waste = 1e9;
+  for (int g = 1; g * p->z <= 512; ++g) {
+    if (smem_for(g, lb, mb) > smem_max) break;
+    const int thr = g * p->z;
+    const int thr32 = (thr + 31) / 32 * 32;
+    const double waste = double(thr32 - thr) / thr32;
+    if (thr32 < 64 && (g + 1) * p->z <= 512 && smem_for(g + 1, lb, mb) <= smem_max) continue;
+    if (waste < best_waste - 1e-9) {
+      best_waste = waste;
+      best_g = g;
+    }
+    if (waste <= 1.0 / 16) break;
+  }
+  p->lanes = lanes;
+  p->groups = best_g;
+  p->threads = (best_g * p->z + 31) / 32 * 32;
+  p->smem = smem_for(best_g, lb, mb);
+  p->kp.groups = best_g;
+  p->kp.l_bytes = (uint32_t)lb;
+  p->kp.m_bytes = (uint32_t)mb;
+  p->kp.m_stride = (uint32_t)(e_pad * lanes);
+  p->kp.magic = 0x64646464u;
+  p->kp.one = 0x3C003C00u;
+  for (int e = 0; e < p->n_edges; ++e) {
+    p->kp.shift_l[e] = (uint16_t)(p->kp.shift_l[e] * lanes);
+    p->kp.colbase[e] = p->kp.colbase[e] * (uint32_t)p->z * lanes;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* nrldpc_last_error(void) { return g_last_error.c_str(); }
+
+int nrldpc_alu_peak(int device, double* alu_lane_ops_per_s, double* mixed_lane_ops_per_s) {
+  NR_CUDA(cudaSetDevice(device));
+  int sms = 0;
+  NR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  uint32_t* d_out = nullptr;
+  NR_CUDA(cudaMalloc(&d_out, 16));
+  cudaEvent_t e0, e1;
+  NR_CUDA(cudaEventCreate(&e0));
+  NR_CUDA(cudaEventCreate(&e1));
+  const int threads = 512, blocks = sms * 4, iters = 4096;
+  double res[2] = {0, 0};
+  for (int mixed = 0; mixed < 2; ++mixed) {
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+      NR_CUDA(cudaEventRecord(e0));
+      if (mixed) k_alu_peak<true><<<blocks, threads>>>(d_out, iters, 0x1234u + rep);
+      else k_alu_peak<false><<<blocks, threads>>>(d_out, iters, 0x1234u + rep);
+      NR_CUDA(cudaEventRecord(e1));
+      NR_CUDA(cudaEventSynchronize(e1));
+      float ms = 0;
+      NR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      if (rep > 0) best = std::min(best, ms);
+    }
+    // two half2 instructions per chain step, 8 chains, iters steps, per thread
+    const double lane_ops = 2.0 * 8.0 * iters * (double)threads * blocks;
+    res[mixed] = lane_ops / (best * 1e-3);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d_out);
+  if (alu_lane_ops_per_s) *alu_lane_ops_per_s = res[0];
+  if (mixed_lane_ops_per_s) *mixed_lane_ops_per_s = res[1];
+  return NRLDPC_OK;
+}
+
+int nrldpc_launch_count(void) { return g_launches; }
+
+int nrldpc_plan_create(int device, int k_b, int z, int rows_used, const int32_t* row_start,
+                       const int16_t* cols, const int16_t* shifts, int precision, double beta,
+                       int max_iter, int early_stop, int crc_kind, nrldpc_plan** out) {
+  if (!out) return fail(NRLDPC_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!row_start || !cols || !shifts) return fail(NRLDPC_EINVAL, "graph tables are NULL");
+  if (z < 2 || z > 384) return fail(NRLDPC_EINVAL, "Z must be in [2, 384]");
+  if (k_b != 22 && k_b != 10) return fail(NRLDPC_EINVAL, "k_b must be 22 (BG1) or 10 (BG2)");
+  if (rows_used < 4 || rows_used > NR_MAX_ROWS)
+    return fail(NRLDPC_EINVAL, "rows_used must be in [4, 46]");
+  if (!(beta > 0.0 && beta <= 1.0)) return fail(NRLDPC_EINVAL, "beta must be in (0, 1]");
+  if (max_iter < 1) return fail(NRLDPC_EINVAL, "max_iter must be at least 1");
+  if (precision != NRLDPC_INT8)
+    return fail(NRLDPC_EINVAL, "only int8 precision is implemented on the device path");
+  if (early_stop < NRLDPC_STOP_SYNDROME || early_stop > NRLDPC_STOP_NONE)
+    return fail(NRLDPC_EINVAL, "unknown early_stop mode");
+  int crc_len = 0;
+  uint32_t crc_poly = 0;
+  if (crc_params(crc_kind, &crc_len, &crc_poly) != 0) return fail(NRLDPC_EINVAL, "unknown crc kind");
+  const int n_edges = row_start[rows_used];
+  if (row_start[0] != 0 || n_edges <= 0 || n_edges > NR_MAX_EDGES)
+    return fail(NRLDPC_EINVAL, "bad row_start table");
+  const int n_blocks = k_b + rows_used;
+  int maxw = 0;
+  for (int r = 0; r < rows_used; ++r) {
+    const int w = row_start[r + 1] - row_start[r];
+    if (w < 2 || w > 19) return fail(NRLDPC_EINVAL, "row weight must be in [2, 19]");
+    maxw = std::max(maxw, w);
+  }
+  for (int e = 0; e < n_edges; ++e) {
+    if (cols[e] < 0 || cols[e] >= n_blocks) return fail(NRLDPC_EINVAL, "edge column out of range");
+    if (shifts[e] < 0 || shifts[e] >= z) return fail(NRLDPC_EINVAL, "edge shift must be in [0, Z)");
+  }
+  int ndev = 0;
+  cudaError_t ce = cudaGetDeviceCount(&ndev);
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaGetDeviceCount");
+  if (device < 0 || device >= ndev) return fail(NRLDPC_EINVAL, "device index out of range");
+
+  nrldpc_plan* p = new (std::nothrow) nrldpc_plan();
+  if (!p) return fail(NRLDPC_ENOMEM, "plan allocation failed");
+  p->device = device;
+  p->precision = precision;
+  p->early_stop = early_stop;
+  p->crc_kind = crc_kind;
+  p->beta = beta;
+  p->max_iter = max_iter;
+  p->k_b = k_b;
+  p->z = z;
+  p->rows = rows_used;
+  p->n_blocks = n_blocks;
+  p->n_edges = n_edges;
+  p->maxw = maxw;
+  KParams& kp = p->kp;
+  std::memset(&kp, 0, sizeof(kp));
+  kp.z = z;
+  kp.k_b = k_b;
+  kp.rows = rows_used;
+  kp.n_blocks = n_blocks;
+  kp.n_edges = n_edges;
+  kp.max_iter = max_iter;
+  kp.early_stop = early_stop;
+  kp.crc_len = crc_len;
+  kp.crc_poly = crc_poly;
+  kp.words = (k_b * z + 31) / 32;
+  for (int r = 0; r <= rows_used; ++r) kp.row_start[r] = (uint16_t)row_start[r];
+  for (int e = 0; e < n_edges; ++e) {
+    kp.shift_l[e] = (uint16_t)shifts[e];
+    kp.colbase[e] = (uint32_t)cols[e];
+  }
+  // int8 beta rule: floor(beta * m) computed in float64 (decoder.py:208-212)
+  for (int m = 0; m < 128; ++m) kp.lut[m] = float_to_half_bits((float)std::floor(beta * (double)m));
+  choose_shape(p);
+  p->schedule = 0;
+  for (int bg = 1; bg <= 2; ++bg) {
+    const int kb_bg = bg == 1 ? 22 : 10;
+    const int nrows = bg == 1 ? RowW<1>::n : RowW<2>::n;
+    if (k_b != kb_bg || rows_used > nrows) continue;
+    bool same = true;
+    for (int r = 0; r <= rows_used && same; ++r)
+      same = row_start[r] == (bg == 1 ? RowW<1>::e0[r] : RowW<2>::e0[r]);
+    if (same) p->schedule = bg;
+  }
+  *out = p;
+  return NRLDPC_OK;
+}
+
+int nrldpc_plan_destroy(nrldpc_plan* plan) {
+  if (!plan) return NRLDPC_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(plan->device);
+  for (auto& s : plan->streams)
+    if (s) cudaStreamDestroy(s);
+  if (plan->d_buf) cudaFree(plan->d_buf);
+  cudaSetDevice(prev);
+  delete plan;
+  return NRLDPC_OK;
+}
+
+int nrldpc_plan_info(const nrldpc_plan* plan, int64_t* k, int64_t* n_c, int64_t* n_tx,
+                     int64_t* words_per_cw, int* lanes, int* groups_per_cta, int* threads_per_cta,
+                     int64_t* smem_bytes) {
+  if (!plan) return fail(NRLDPC_EINVAL, "plan is NULL");
+  if (k) *k = (int64_t)plan->k_b * plan->z;
+  if (n_c) *n_c = (int64_t)plan->n_blocks * plan->z;
+  if (n_tx) *n_tx = (int64_t)(plan->n_blocks - 2) * plan->z;
+  if (words_per_cw) *words_per_cw = plan->kp.words;
+  if (lanes) *lanes = plan->lanes;
+  if (groups_per_cta) *groups_per_cta = plan->groups;
+  if (threads_per_cta) *threads_per_cta = plan->threads;
+  if (smem_bytes) *smem_bytes = (int64_t)plan->smem;
+  return NRLDPC_OK;
+}
+
+int nrldpc_quantize(const nrldpc_plan* plan, const void* llr_in, int in_dtype, int64_t batch,
+                    double scale, double clip, void* out, int out_mode, void* stream) {
+  g_launches = 0;
+  if (!plan) return fail(NRLDPC_EINVAL, "plan is NULL");
+  if (batch < 0) return fail(NRLDPC_EINVAL, "batch must be non-negative");
+  if (!(scale > 0.0)) return fail(NRLDPC_EINVAL, "scale must be positive");
+  if (batch == 0) return NRLDPC_OK;
+  if (!llr_in || !out) return fail(NRLDPC_EINVAL, "NULL buffer");
+  const int n_c = plan->n_blocks * plan->z;
+  const int n_tx = n_c - 2 * plan->z;
+  cudaStream_t st = (cudaStream_t)stream;
+  NR_CUDA(cudaSetDevice(plan->device));
+  const long long total = batch * (long long)n_c;
+  const long long want = (total + 4 * 256 - 1) / (4 * 256);
+  const int grid = (int)std::min<long long>(want, 148LL * 16);
+  auto go = [&](auto kern, auto* typed_in) {
+    kern<<<grid, 256, 0, st>>>(typed_in, (long long)batch, n_tx, n_c, 2 * plan->z, scale, clip, out);
+  };
+  if (in_dtype == NRLDPC_IN_F64) {
+    const double* in = static_cast<const double*>(llr_in);
+    if (out_mode == NRLDPC_INT8) go(k_quantize<double, NRLDPC_INT8>, in);
+    else if (out_mode == NRLDPC_F16) go(k_quantize<double, NRLDPC_F16>, in);
+    else if (out_mode == NRLDPC_F32) go(k_quantize<double, NRLDPC_F32>, in);
+    else return fail(NRLDPC_EINVAL, "unknown quantize out_mode");
+  } else if (in_dtype == NRLDPC_IN_F32) {
+    const float* in = static_cast<const float*>(llr_in);
+    if (out_mode == NRLDPC_INT8) go(k_quantize<float, NRLDPC_INT8>, in);
+    else if (out_mode == NRLDPC_F16) go(k_quantize<float, NRLDPC_F16>, in);
+    else if (out_mode == NRLDPC_F32) go(k_quantize<float, NRLDPC_F32>, in);
+    else return fail(NRLDPC_EINVAL, "unknown quantize out_mode");
+  } else {
+    return fail(NRLDPC_EINVAL, "unknown quantize input dtype");
+  }
+  ++g_launches;
+  NR_CUDA(cudaGetLastError());
+  return NRLDPC_OK;
+}
+
+static int decode_impl(const nrldpc_plan* plan, const void* llr, int64_t batch, const KOut& o,
+                       cudaStream_t st) {
+  cudaError_t e = cudaSuccess;
+  if (plan->precision == NRLDPC_INT8) {
+    const int8_t* in = static_cast<const int8_t*>(llr);
+    const bool two = plan->lanes == 2;
+    switch (plan->schedule) {
+      case 1: e = two ? launch_i8<1, 19, 2>(plan, in, batch, o, st) : launch_i8<1, 19, 1>(plan, in, batch, o, st); break;
+      case 2: e = two ? launch_i8<2, 10, 2>(plan, in, batch, o, st) : launch_i8<2, 10, 1>(plan, in, batch, o, st); break;
+      default:
+        if (plan->maxw > 10)
+          e = two ? launch_i8<0, 19, 2>(plan, in, batch, o, st) : launch_i8<0, 19, 1>(plan, in, batch, o, st);
+        else
+          e = two ? launch_i8<0, 10, 2>(plan, in, batch, o, st) : launch_i8<0, 10, 1>(plan, in, batch, o, st);
+    }
+  } else {
+    return fail(NRLDPC_EINVAL, "precision not implemented");
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "decode launch");
+  return NRLDPC_OK;
+}
+
+int nrldpc_decode(const nrldpc_plan* plan, const void* llr, int64_t batch, uint32_t* bits,
+                  int32_t* iters, int32_t* synd, uint8_t* success, uint8_t* crc_ok, int32_t* trace_w,
+                  float* trace_m, int32_t* status, void* stream) {
+  g_launches = 0;
+  if (!plan) return fail(NRLDPC_EINVAL, "plan is NULL");
+  if (batch < 0) return fail(NRLDPC_EINVAL, "batch must be non-negative");
+  if (batch == 0) return NRLDPC_OK;
+  if (!llr || !bits || !iters || !synd || !success) return fail(NRLDPC_EINVAL, "NULL buffer");
+  if ((trace_w == nullptr) != (trace_m == nullptr))
+    return fail(NRLDPC_EINVAL, "trace_w and trace_m must both be set or both NULL");
+  if (plan->early_stop == NRLDPC_STOP_CRC && !crc_ok)
+    return fail(NRLDPC_EINVAL, "crc mode needs a crc_ok buffer");
+  NR_CUDA(cudaSetDevice(plan->device));
+  KOut o{bits, iters, synd, success, crc_ok, trace_w, trace_m, status};
+  return decode_impl(plan, llr, batch, o, (cudaStream_t)stream);
+}
+
+int nrldpc_decode_host(nrldpc_plan* plan, const void* llr_host, int64_t batch, uint32_t* bits,
+                       int32_t* iters, int32_t* synd, uint8_t* success, uint8_t* crc_ok, int chunks) {
+  g_launches = 0;
+  if (!plan) return fail(NRLDPC_EINVAL, "plan is NULL");
+  if (batch < 0) return fail(NRLDPC_EINVAL, "batch must be non-negative");
+  if (batch == 0) return NRLDPC_OK;
+  if (!llr_host || !bits || !iters || !synd || !success) return fail(NRLDPC_EINVAL, "NULL buffer");
+  if (plan->early_stop == NRLDPC_STOP_CRC && !crc_ok)
+    return fail(NRLDPC_EINVAL, "crc mode needs a crc_ok buffer");
+  std::lock_guard<std::mutex> lock(plan->host_mu);
+  NR_CUDA(cudaSetDevice(plan->device));
+  const size_t esz = plan->precision == NRLDPC_INT8 ? 1 : (plan->precision == NRLDPC_F16 ? 2 : 4);
+  const size_t n_c = (size_t)plan->n_blocks * plan->z;
+  const size_t words = plan->kp.words;
+  const size_t per_cw_in = n_c * esz;
+  const size_t per_cw_out = words * 4 + 4 + 4 + 1 + 1;
+  const size_t need = align16(batch * per_cw_in) + align16(batch * words * 4) + align16(batch * 4) * 2 +
+                      align16(batch) * 2 + 16;
+  if (need > plan->d_cap) {
+    if (plan->d_buf) cudaFree(plan->d_buf);
+    plan->d_buf = nullptr;
+    plan->d_cap = 0;
+    NR_CUDA(cudaMalloc(&plan->d_buf, need));
+    plan->d_cap = need;
+  }
+  (void)per_cw_out;
+  for (auto& s : plan->streams)
+    if (!s) NR_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  uint8_t* base = static_cast<uint8_t*>(plan->d_buf);
+  uint8_t* d_llr = base;
+  uint32_t* d_bits = reinterpret_cast<uint32_t*>(base + align16(batch * per_cw_in));
+  int32_t* d_iters = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(d_bits) + align16(batch * words * 4));
+  int32_t* d_synd = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(d_iters) + align16(batch * 4));
+  uint8_t* d_succ = reinterpret_cast<uint8_t*>(d_synd) + align16(batch * 4);
+  uint8_t* d_crc = d_succ + align16(batch);
+  int32_t* d_status = reinterpret_cast<int32_t*>(d_crc + align16(batch));
+  NR_CUDA(cudaMemsetAsync(d_status, 0, 4, plan->streams[0]));
+  NR_CUDA(cudaStreamSynchronize(plan->streams[0]));
+  if (chunks < 1) chunks = 1;
+  const int64_t per_lane_cta = (int64_t)plan->groups * plan->lanes;
+  int64_t chunk = (batch + chunks - 1) / chunks;
+  chunk = (chunk + per_lane_cta - 1) / per_lane_cta * per_lane_cta;
+  int launches = 0;
+  int idx = 0;
+  for (int64_t b0 = 0; b0 < batch; b0 += chunk, ++idx) {
+    const int64_t nb = std::min<int64_t>(chunk, batch - b0);
+    cudaStream_t st = plan->streams[idx % 3];
+    NR_CUDA(cudaMemcpyAsync(d_llr + b0 * per_cw_in, static_cast<const uint8_t*>(llr_host) + b0 * per_cw_in,
+                            nb * per_cw_in, cudaMemcpyHostToDevice, st));
+    KOut o{d_bits + b0 * words, d_iters + b0, d_synd + b0, d_succ + b0,
+           crc_ok ? d_crc + b0 : nullptr, nullptr, nullptr, d_status};
+    const int rc = decode_impl(plan, d_llr + b0 * per_cw_in, nb, o, st);
+    if (rc != NRLDPC_OK) return rc;
+    launches += g_launches;
+    NR_CUDA(cudaMemcpyAsync(bits + b0 * words, d_bits + b0 * words, nb * words * 4, cudaMemcpyDeviceToHost, st));
+    NR_CUDA(cudaMemcpyAsync(iters + b0, d_iters + b0, nb * 4, cudaMemcpyDeviceToHost, st));
+    NR_CUDA(cudaMemcpyAsync(synd + b0, d_synd + b0, nb * 4, cudaMemcpyDeviceToHost, st));
+    NR_CUDA(cudaMemcpyAsync(success + b0, d_succ + b0, nb, cudaMemcpyDeviceToHost, st));
+    if (crc_ok) NR_CUDA(cudaMemcpyAsync(crc_ok + b0, d_crc + b0, nb, cudaMemcpyDeviceToHost, st));
+  }
+  int32_t status = 0;
+  for (auto& s : plan->streams) NR_CUDA(cudaStreamSynchronize(s));
+  NR_CUDA(cudaMemcpy(&status, d_status, 4, cudaMemcpyDeviceToHost));
+  g_launches = launches;
+  if (status) return fail(NRLDPC_EINVAL, "int8 LLR magnitudes must be at most 127");
+  return NRLDPC_OK;
+}
+
+}  // extern "C"

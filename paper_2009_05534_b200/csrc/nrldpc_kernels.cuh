@@ -1,0 +1,128 @@
+// Device-side building blocks shared by the nrldpc kernels (sm_100a).
+//
+// Exact int8 layered min-sum in packed half2 arithmetic
+// -----------------------------------------------------
+// The reference's int8 engine (/root/reference/pkg/src/ldpclab/decoder.py:
+// 295-320) widens int8 posteriors L and messages M to int32 and computes
+//     t   = clamp127(L - M)          (decoder.py:300)
+//     m1, m2, S over |t|, sign(t)    (decoder.py:305, kernels.py:246-257)
+//     b   = floor(beta * m)          (decoder.py:208-212)
+//     out = (S ^ sign t) ? -b : b    (decoder.py:315-316)
+//     L'  = clamp127(t + out)        (decoder.py:318)
+// Every intermediate is an integer with |x| <= 254, so IEEE half represents
+// it exactly and HADD2/HFMA2/HMNMX2 reproduce the integer results bit for
+// bit. Two codewords ride in the two half lanes of one 32-bit register
+// (LANES=2), so one SASS instruction does the work of two codeword-edges;
+// |x| comes for free as an HMNMX2 operand modifier.
+//
+// Storage is one biased byte per value and codeword: u = v + 128 (the int8
+// bit pattern with the top bit flipped). One PRMT with the byte 0x64 turns a
+// pair of stored bytes into the half2 {1024+u_a, 1024+u_b} = {1152+v_a,
+// 1152+v_b}; subtracting two such values yields the exact unbiased t, and
+// HFMA2(y, +-1, 1152) maps a result back into the same biased form, whose
+// low byte is again u. The bias also makes a -0.0 result impossible to store.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#define NR_MAX_ROWS 46
+#define NR_MAX_EDGES 316
+#define NR_MAX_BLOCKS 68
+
+namespace nr {
+
+struct KParams {
+  int z;
+  int k_b;
+  int rows;          // rows_used
+  int n_blocks;      // k_b + rows_used
+  int n_edges;       // sum of w_r over the used rows
+  int groups;        // codeword groups per CTA (a group = Z threads)
+  int max_iter;
+  int early_stop;    // NRLDPC_STOP_*
+  int crc_len;
+  uint32_t crc_poly;
+  int trace;         // nonzero: record per-iteration trace, never exit early
+  int words;         // ceil(K/32)
+  long long batch;
+  uint32_t l_bytes;  // per group: n_blocks*z*LANES rounded up to 16
+  uint32_t m_bytes;  // per group: z * m_stride rounded up to 16
+  uint32_t m_stride; // bytes between consecutive z message rows (odd # words)
+  uint32_t magic;    // 0x64646464: PRMT filler byte (half exponent of 1024)
+  uint32_t one;      // 0x3C003C00: half2 {1.0, 1.0}
+  uint16_t row_start[NR_MAX_ROWS + 1];
+  uint16_t shift_l[NR_MAX_EDGES];   // shift * LANES (bytes)
+  uint32_t colbase[NR_MAX_EDGES];   // col * z * LANES (bytes)
+  uint16_t lut[128];                // floor(beta*m) as half bits, m = 0..127
+};
+
+struct KOut {
+  uint32_t* bits;
+  int32_t* iters;
+  int32_t* synd;
+  uint8_t* success;
+  uint8_t* crc_ok;
+  int32_t* trace_w;
+  float* trace_m;
+  int32_t* status;
+};
+
+__device__ __forceinline__ uint32_t h2u(half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+__device__ __forceinline__ half2 u2h(uint32_t u) { return *reinterpret_cast<half2*>(&u); }
+
+// biased byte(s) -> half2 {1152+v_a, 1152+v_b}
+// `magic` must hold 0x64646464 in a register (kept opaque so ptxas puts the
+// selector, not the constant, in PRMT's immediate slot).
+template <int LANES>
+__device__ __forceinline__ half2 unpack_elem(uint32_t raw, uint32_t magic) {
+  uint32_t d;
+  if (LANES == 2)
+    asm("prmt.b32 %0, %1, %2, 0x4140;" : "=r"(d) : "r"(raw), "r"(magic));
+  else
+    asm("prmt.b32 %0, %1, %2, 0x4040;" : "=r"(d) : "r"(raw), "r"(magic));
+  return u2h(d);
+}
+
+// biased half2 -> stored byte(s) (low byte of each lane)
+template <int LANES>
+__device__ __forceinline__ uint32_t pack_elem(half2 h) {
+  return LANES == 2 ? __byte_perm(h2u(h), 0, 0x0020) : h2u(h);
+}
+
+template <int LANES>
+__device__ __forceinline__ uint32_t ld_elem(const uint8_t* p) {
+  if (LANES == 2) return *reinterpret_cast<const uint16_t*>(p);
+  return *p;
+}
+
+template <int LANES>
+__device__ __forceinline__ void st_elem(uint8_t* p, uint32_t v) {
+  if (LANES == 2) *reinterpret_cast<uint16_t*>(p) = (uint16_t)v;
+  else *p = (uint8_t)v;
+}
+
+// Predicated shared store (no branch): padding threads compute but never
+// store. All loads of a row precede its stores through register
+// dependences (every stored value depends on m1/m2/S of the whole row),
+// and rows are separated by __syncthreads, so no memory clobber is needed.
+template <int LANES>
+__device__ __forceinline__ void st_elem_if(uint8_t* p, uint32_t v, bool ok) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+  if (LANES == 2)
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.u16 [%0], %1; }" ::"r"(a), "h"((uint16_t)v),
+                 "r"((uint32_t)ok));
+  else
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.u8 [%0], %1; }" ::"r"(a), "h"((uint16_t)v),
+                 "r"((uint32_t)ok));
+}
+
+// beta LUT on a half2 of integer magnitudes 0..127
+__device__ __forceinline__ half2 beta_lut2(const uint16_t* lut, half2 m) {
+  const uint32_t x = h2u(__hadd2(m, u2h(0x64006400u)));  // lanes 0x6400|m
+  const uint32_t lo = lut[x & 0x7Fu];
+  const uint32_t hi = lut[(x >> 16) & 0x7Fu];
+  return u2h(lo | (hi << 16));
+}
+
+}  // namespace nr

@@ -1,0 +1,197 @@
+"""GPU parity: the sm_100a decoder (through the C ABI) against the reference's
+golden vectors and against the pinned C oracle at full BASELINE sizes.
+
+Bar: bit-exact bits, iterations, success, syndrome weight, crc_ok and trace
+(int8 fixed-point path).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2009_05534_b200 as nr
+from paper_2009_05534_b200 import _native
+from paper_2009_05534_b200.synth import noisy_llrs
+from oracle import oracle
+from tests.golden_cases import load_cases, make_cfg
+
+pytestmark = pytest.mark.gpu
+
+INT8_CASES = sorted(n for n, c in load_cases()["cases"].items() if c.cfg["precision"] == "int8")
+
+
+def assert_same(res, ref_bits, ref_iters, ref_succ, ref_synd, ref_crc=None):
+    assert res.bits.shape == ref_bits.shape
+    bad = np.flatnonzero((res.bits != ref_bits).any(axis=1))
+    assert bad.size == 0, f"bits differ in codewords {bad[:10]}"
+    assert np.array_equal(res.iterations, ref_iters), (res.iterations, ref_iters)
+    assert np.array_equal(res.success, ref_succ)
+    assert np.array_equal(res.syndrome_weight, ref_synd)
+    if ref_crc is not None:
+        assert np.array_equal(res.crc_ok, ref_crc)
+
+
+@pytest.mark.parametrize("name", INT8_CASES)
+def test_golden_int8(cuda_ok, name):
+    case = load_cases()["cases"][name]
+    bg = nr.load_basegraph(case.bg, case.z)
+    cfg = make_cfg(case, nr.DecodeConfig)
+    trace = [] if case.trace else None
+    res = nr.decode(case.llr, bg, cfg, trace)
+    crc = case.arrays["crc_ok"].astype(bool) if "crc_ok" in case.arrays else None
+    assert_same(res, case.bits(), case.arrays["iterations"], case.arrays["success"].astype(bool),
+                case.arrays["syndrome_weight"], crc)
+    if case.trace:
+        assert trace == case.trace_list()
+
+
+def test_golden_quantize(cuda_ok):
+    q = load_cases()["quant"]
+    bg = nr.load_basegraph("BG2", 16)
+    params = nr.code_params(bg, 16, 42)
+    for mode in ("int8", "f16", "f32"):
+        got = nr.quantize(q["x"], nr.QuantConfig(mode=mode), params)
+        assert got.dtype == q[mode].dtype
+        assert np.array_equal(got.view(np.uint8), q[mode].view(np.uint8)), mode
+
+
+def test_quantize_device_tensor_f32_input(cuda_ok):
+    bg = nr.load_basegraph("BG1", 384)
+    params = nr.code_params(bg, 384, 46)
+    _, llr = noisy_llrs(bg, 46, 2.0, 8, seed=1)
+    x32 = llr.astype(np.float32)
+    dev = nr.quantize(torch.from_numpy(x32).cuda(), nr.QuantConfig(), params)
+    assert dev.is_cuda and dev.dtype == torch.int8
+    # the reference widens float32 input to float64 before scaling
+    assert np.array_equal(dev.cpu().numpy(), oracle.quantize_i8(x32.astype(np.float64), 384))
+
+
+def _oracle_cmp(bg, rows, cfg, llr_i8, trace=False):
+    tr_ref = [] if trace else None
+    ref = oracle.decode(llr_i8, bg, cfg, tr_ref)
+    tr = [] if trace else None
+    res = nr.decode(llr_i8, bg, cfg, tr)
+    assert_same(res, ref["bits"], ref["iterations"], ref["success"], ref["syndrome_weight"],
+                ref["crc_ok"])
+    if trace:
+        assert tr == tr_ref
+    return res
+
+
+def test_config2_full_batch_vs_oracle(cuda_ok):
+    """BASELINE config 2: BG1 Z=384, B=1024, fixed 10 iterations."""
+    bg = nr.load_basegraph("BG1", 384)
+    _, llr = noisy_llrs(bg, 46, 2.0, 1024, seed=2024)
+    blocks = oracle.quantize_i8(llr, 384)
+    cfg = nr.DecodeConfig(max_iter=10, early_stop="none")
+    res = _oracle_cmp(bg, 46, cfg, blocks)
+    assert (res.iterations == 10).all()
+
+
+def test_config3_early_termination_vs_oracle(cuda_ok):
+    """BASELINE config 3: BG2 Z=384 at 0.5 dB, syndrome stop, max 20."""
+    bg = nr.load_basegraph("BG2", 384)
+    _, llr = noisy_llrs(bg, 42, 0.5, 512, seed=3)
+    blocks = oracle.quantize_i8(llr, 384)
+    res = _oracle_cmp(bg, 42, nr.DecodeConfig(max_iter=20), blocks)
+    assert res.iterations.min() < res.iterations.max()  # variable iteration counts
+
+
+@pytest.mark.parametrize("bg_id", ["BG1", "BG2"])
+def test_config4_every_lifting_size_vs_oracle(cuda_ok, bg_id):
+    """BASELINE config 4 groups: all 51 Z, 16 codewords each, 10 iterations."""
+    for z in nr.ALL_LIFTING_SIZES:
+        bg = nr.load_basegraph(bg_id, z)
+        _, llr = noisy_llrs(bg, bg.m_bg, 2.0, 16, seed=(int(bg_id[-1]), z, 4))
+        blocks = oracle.quantize_i8(llr, z)
+        _oracle_cmp(bg, bg.m_bg, nr.DecodeConfig(max_iter=10, early_stop="none"), blocks)
+        _oracle_cmp(bg, bg.m_bg, nr.DecodeConfig(max_iter=10), blocks)
+
+
+@pytest.mark.parametrize("batch", [1, 2, 3, 5, 33, 149, 301])
+def test_ragged_batches(cuda_ok, batch):
+    """Batches that leave half-filled lane pairs / groups / CTAs."""
+    for bg_id, z in (("BG2", 16), ("BG1", 7), ("BG1", 384), ("BG2", 240)):
+        bg = nr.load_basegraph(bg_id, z)
+        _, llr = noisy_llrs(bg, bg.m_bg, 1.5, batch, seed=(batch, z))
+        blocks = oracle.quantize_i8(llr, z)
+        _oracle_cmp(bg, bg.m_bg, nr.DecodeConfig(max_iter=8), blocks)
+
+
+def test_empty_batch(cuda_ok):
+    bg = nr.load_basegraph("BG2", 16)
+    res = nr.decode(np.zeros((0, 832), np.int8), bg, nr.DecodeConfig())
+    assert res.bits.shape == (0, 160) and res.iterations.shape == (0,)
+
+
+@pytest.mark.parametrize("rows", [4, 5, 17, 30, 45])
+def test_partial_rows_vs_oracle(cuda_ok, rows):
+    for bg_id, z in (("BG1", 384), ("BG2", 44)):
+        bg = nr.load_basegraph(bg_id, z)
+        if rows > bg.m_bg:
+            continue
+        _, llr = noisy_llrs(bg, rows, 2.5, 24, seed=(rows, z))
+        _oracle_cmp(bg, rows, nr.DecodeConfig(max_iter=12), oracle.quantize_i8(llr, z))
+
+
+@pytest.mark.parametrize("beta", [0.75, 0.5, 1.0, 0.8, 0.3, 0.6875])
+def test_beta_values_vs_oracle(cuda_ok, beta):
+    bg = nr.load_basegraph("BG1", 104)
+    _, llr = noisy_llrs(bg, 46, 1.75, 64, seed=int(beta * 1000))
+    _oracle_cmp(bg, 46, nr.DecodeConfig(max_iter=15, beta=beta), oracle.quantize_i8(llr, 104))
+
+
+def test_trace_and_crc_vs_oracle(cuda_ok):
+    bg = nr.load_basegraph("BG1", 64)
+    params = nr.code_params(bg, 64, 46)
+    rng = np.random.default_rng(12)
+    msgs = np.stack([nr.crc_attach(rng.integers(0, 2, params.k - 24, dtype=np.uint8), k=params.k)
+                     for _ in range(40)])
+    tx = nr.encode_batch(msgs, bg, 64, 46)[:, 128:]
+    sigma = nr.ebn0_to_sigma(1.5, params.k / params.n_tx)
+    llr = nr.demap_llr(nr.bpsk_awgn(tx, sigma, rng), sigma)
+    blocks = oracle.quantize_i8(llr, 64)
+    _oracle_cmp(bg, 46, nr.DecodeConfig(max_iter=12, early_stop="crc"), blocks, trace=True)
+    _oracle_cmp(bg, 46, nr.DecodeConfig(max_iter=12, early_stop="crc", rho=4), blocks, trace=True)
+    _oracle_cmp(bg, 46, nr.DecodeConfig(max_iter=7, early_stop="none"), blocks, trace=True)
+
+
+def test_saturated_inputs_and_erasures(cuda_ok):
+    """+-127 everywhere, all-zero blocks and mixed erasures."""
+    bg = nr.load_basegraph("BG1", 384)
+    rng = np.random.default_rng(9)
+    blocks = rng.choice(np.array([-127, 127, 0], np.int8), size=(6, 26112))
+    blocks[0] = 0
+    blocks[1] = 127
+    blocks[2] = -127
+    _oracle_cmp(bg, 46, nr.DecodeConfig(max_iter=6), blocks)
+    _oracle_cmp(bg, 46, nr.DecodeConfig(max_iter=6, early_stop="none"), blocks, trace=True)
+
+
+def test_device_tensor_input_and_host_path_agree(cuda_ok):
+    bg = nr.load_basegraph("BG1", 384)
+    _, llr = noisy_llrs(bg, 46, 2.0, 70, seed=77)
+    blocks = oracle.quantize_i8(llr, 384)
+    cfg = nr.DecodeConfig(max_iter=10, early_stop="none")
+    a = nr.decode(blocks, bg, cfg)
+    b = nr.decode(torch.from_numpy(blocks).cuda(), bg, cfg)
+    assert np.array_equal(a.bits, b.bits) and np.array_equal(a.iterations, b.iterations)
+    plan = nr.get_plan(bg, 46, cfg)
+    h = plan.decode_host(blocks, chunks=3)
+    assert np.array_equal(nr.unpack_bits(h["bits"], plan.k), a.bits)
+    assert np.array_equal(h["iters"], a.iterations)
+    assert np.array_equal(h["synd"], a.syndrome_weight)
+
+
+def test_out_of_range_device_input_raises(cuda_ok):
+    bg = nr.load_basegraph("BG2", 16)
+    x = torch.zeros((2, 832), dtype=torch.int8, device="cuda")
+    x[1, 17] = -128
+    with pytest.raises(ValueError, match="at most 127"):
+        nr.decode(x, bg, nr.DecodeConfig())
+
+
+def test_native_library_is_the_compute_path(cuda_ok):
+    bg = nr.load_basegraph("BG2", 64)
+    nr.decode(np.zeros((4, 3328), np.int8), bg, nr.DecodeConfig(max_iter=2))
+    assert _native.launch_count() >= 1

@@ -1,0 +1,180 @@
+"""CPU-side tests: base graphs, synthetic traffic, config/input validation,
+and the C-ABI library surface (no compute calls without a GPU)."""
+
+import ctypes
+import json
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2009_05534_b200 as nr
+from paper_2009_05534_b200 import _native
+from paper_2009_05534_b200.synth import noisy_llrs
+from oracle import oracle
+from tests.golden_cases import load_cases
+
+ROOT = Path(__file__).resolve().parents[1]
+REF_ASSETS = Path("/root/reference/pkg/src/ldpclab/assets")
+
+
+# --- base graphs (basegraph.py:22-236) ---------------------------------------
+
+def test_lifting_sets():
+    assert len(nr.ALL_LIFTING_SIZES) == 51
+    assert nr.ALL_LIFTING_SIZES[0] == 2 and nr.ALL_LIFTING_SIZES[-1] == 384
+    assert nr.lifting_set_index(384) == 1
+    with pytest.raises(ValueError, match="not a valid lifting size"):
+        nr.lifting_set_index(17)
+
+
+@pytest.mark.parametrize("bg_id,k_b,m_bg,n_ent", [("BG1", 22, 46, 316), ("BG2", 10, 42, 197)])
+def test_graph_dimensions(bg_id, k_b, m_bg, n_ent):
+    bg = nr.load_basegraph(bg_id, 384)
+    assert (bg.k_b, bg.m_bg, bg.n_entries) == (k_b, m_bg, n_ent)
+    assert int(bg.w_r.sum()) == n_ent and bg.w_r.min() >= 3
+    for r in range(bg.m_bg):
+        cols, shifts = bg.row_entries(r)
+        assert np.all(np.diff(cols) > 0) and np.all((shifts >= 0) & (shifts < 384))
+
+
+def test_asset_provenance_matches_reference_csv():
+    prov = json.loads((ROOT / "paper_2009_05534_b200/assets/provenance.json").read_text())
+    assert prov["bg1"]["source_sha256"].startswith("8e3ea207")
+    assert prov["bg2"]["source_sha256"].startswith("5e16acb7")
+    if not REF_ASSETS.is_dir():
+        pytest.skip("reference assets not mounted (GPU box)")
+    import hashlib
+    for name in ("bg1", "bg2"):
+        blob = (REF_ASSETS / f"{name}.csv").read_bytes()
+        assert hashlib.sha256(blob).hexdigest() == prov[name]["source_sha256"]
+        raw = np.loadtxt(REF_ASSETS / f"{name}.csv", dtype=np.int64, delimiter=",", skiprows=1)
+        for z in (2, 15, 104, 384):
+            bg = nr.load_basegraph(name.upper(), z)
+            shifts = np.mod(raw[:, 2 + nr.lifting_set_index(z)], z)
+            order = np.lexsort((raw[:, 1], raw[:, 0]))
+            assert np.array_equal(bg.cols, raw[order, 1])
+            assert np.array_equal(bg.shifts, shifts[order])
+
+
+def test_code_params():
+    bg = nr.load_basegraph("BG1", 384)
+    p = nr.code_params(bg, 384, 46)
+    assert (p.k, p.n_c, p.n_tx) == (8448, 26112, 25344)
+    with pytest.raises(ValueError, match="rows_used"):
+        nr.code_params(bg, 384, 3)
+
+
+# --- synthetic traffic == the reference's make_noisy_blocks -------------------
+
+@pytest.mark.parametrize("name,bg_id,z,rows,ebn0,count,seed", [
+    ("bg2_z16_syn12", "BG2", 16, 42, 1.5, 64, 7),
+    ("cfg2_bg1_z384_none10", "BG1", 384, 46, 2.0, 6, 2024),
+    ("bg1_z8_rows8", "BG1", 8, 8, 3.0, 16, 60),
+    ("bg1_z15_syn20", "BG1", 15, 46, 2.0, 8, (15, 46)),
+])
+def test_synthetic_llrs_match_reference_fixture(name, bg_id, z, rows, ebn0, count, seed):
+    case = load_cases()["cases"][name]
+    _, llr = noisy_llrs(nr.load_basegraph(bg_id, z), rows, ebn0, count, seed)
+    assert np.array_equal(oracle.quantize_i8(llr, z), case.llr)
+
+
+def test_encoder_codewords_satisfy_all_checks():
+    rng = np.random.default_rng(5)
+    for bg_id in ("BG1", "BG2"):
+        for z in (2, 3, 13, 384):
+            bg = nr.load_basegraph(bg_id, z)
+            for rows in (4, bg.m_bg):
+                msgs = rng.integers(0, 2, size=(3, bg.k_b * z), dtype=np.uint8)
+                cw = nr.encode_batch(msgs, bg, z, rows)
+                assert np.array_equal(cw[:, : bg.k_b * z], msgs)
+                assert not nr.syndrome_weights(cw, bg, rows).any()
+
+
+def test_crc_attach_check_roundtrip():
+    rng = np.random.default_rng(3)
+    for kind in ("crc24a", "crc24b", "crc16"):
+        payload = rng.integers(0, 2, 100, dtype=np.uint8)
+        msg = nr.crc_attach(payload, kind)
+        assert nr.crc_check(msg, kind)
+        msg[7] ^= 1
+        assert not nr.crc_check(msg, kind)
+
+
+# --- config / input validation (decoder.py:62-85, 261-267, 287-288, 555-557) ---
+
+def test_config_validation_messages():
+    with pytest.raises(ValueError, match=r"beta must be in \(0, 1\]"):
+        nr.DecodeConfig(beta=0.0)
+    with pytest.raises(ValueError, match="max_iter"):
+        nr.DecodeConfig(max_iter=0)
+    with pytest.raises(ValueError, match="power of two"):
+        nr.DecodeConfig(strategy="low_latency", alpha=3)
+    with pytest.raises(ValueError, match="rho=4 is inconsistent"):
+        nr.DecodeConfig(precision="f32", rho=4)
+    with pytest.raises(ValueError):
+        nr.DecodeConfig(precision=nr.Precision.INT8, rho=2)
+    cfg = nr.DecodeConfig()
+    assert (cfg.beta, cfg.max_iter, cfg.rho, cfg.precision, cfg.early_stop) == (
+        0.75, 20, 1, nr.Precision.INT8, nr.EarlyStop.SYNDROME)
+
+
+def test_decode_input_validation_before_any_launch():
+    bg = nr.load_basegraph("BG2", 16)
+    with pytest.raises(ValueError, match="multiple of 4"):
+        nr.decode(np.zeros((3, 832), np.int8), bg, nr.DecodeConfig(rho=4))
+    with pytest.raises(ValueError, match="multiple of Z"):
+        nr.decode(np.zeros(831, np.int8), bg, nr.DecodeConfig())
+    with pytest.raises(ValueError, match="rows_used"):
+        nr.decode(np.zeros(16 * 12, np.int8), bg, nr.DecodeConfig())
+    bad = np.zeros(832, np.int16)
+    bad[3] = 128
+    with pytest.raises(ValueError, match="at most 127"):
+        nr.decode(bad, bg, nr.DecodeConfig())
+
+
+def test_reference_config_objects_are_accepted():
+    # the drop-in takes ldpclab's DecodeConfig (same fields, string enums)
+    class RefLike:
+        beta, max_iter, strategy, alpha, rho = 0.75, 9, "high_throughput", 4, 1
+        precision, early_stop, crc_kind = "int8", "none", "crc24b"
+    from paper_2009_05534_b200.decoder import _coerce_cfg
+    cfg = _coerce_cfg(RefLike())
+    assert cfg.max_iter == 9 and cfg.early_stop is nr.EarlyStop.NONE
+
+
+def test_unpack_bits_lsb_first():
+    words = np.array([[0b1011 | (1 << 31), 0b101]], dtype=np.uint32)
+    bits = nr.unpack_bits(words, 40)
+    assert bits.shape == (1, 40)
+    assert bits[0, :4].tolist() == [1, 1, 0, 1]
+    assert bits[0, 31] == 1 and bits[0, 32:35].tolist() == [1, 0, 1] and bits[0, 35:].sum() == 0
+
+
+# --- the C ABI: library loads and exports every declared entry point ----------
+
+def test_abi_exports_every_header_symbol():
+    header = (ROOT / "include/nrldpc.h").read_text()
+    declared = set(re.findall(r"\b(nrldpc_[a-z_]+)\s*\(", header))
+    assert declared == set(_native.EXPORTS)
+    lib = _native.load()
+    for sym in declared:
+        assert hasattr(lib, sym), sym
+    # error channel works without a GPU
+    assert isinstance(lib.nrldpc_last_error(), bytes)
+
+
+def test_abi_rejects_bad_plans_without_gpu():
+    lib = _native.load()
+    h = ctypes.c_void_p()
+    rs = np.array([0, 3, 6, 9, 12], np.int32)
+    cols = np.zeros(12, np.int16)
+    sh = np.zeros(12, np.int16)
+    rc = lib.nrldpc_plan_create(0, 22, 17 * 0 + 1, 4, rs.ctypes.data, cols.ctypes.data,
+                                sh.ctypes.data, 0, 0.75, 10, 0, 1, ctypes.byref(h))
+    assert rc == _native.NRLDPC_EINVAL
+    assert b"Z must be" in lib.nrldpc_last_error()
+    rc = lib.nrldpc_plan_create(0, 22, 16, 4, rs.ctypes.data, cols.ctypes.data,
+                                sh.ctypes.data, 0, 1.5, 10, 0, 1, ctypes.byref(h))
+    assert rc == _native.NRLDPC_EINVAL and b"beta" in lib.nrldpc_last_error()
