@@ -73,17 +73,46 @@ __device__ __forceinline__ uint32_t edge_offset(const KParams& p, int e, uint32_
   return a + p.colbase[e];
 }
 
+// Message access for one edge. Shared memory: thread-major rows (Mrow =
+// this thread's messages of the current base row, edge j at Mrow + j*LANES).
+// Registers (REGMSG, LANES=2): two 16-bit message pairs per 32-bit register,
+// edge e in half (e & 1) of mreg[e >> 1]; e is a compile-time constant after
+// the schedule is unrolled, so mreg stays in registers.
+template <int LANES, bool REGMSG>
+__device__ __forceinline__ half2 msg_load(const uint8_t* Mrow, const uint32_t* mreg, int j, int e,
+                                          uint32_t magic) {
+  if constexpr (REGMSG) {
+    uint32_t d;
+    if (e & 1) asm("prmt.b32 %0, %1, %2, 0x4342;" : "=r"(d) : "r"(mreg[e >> 1]), "r"(magic));
+    else asm("prmt.b32 %0, %1, %2, 0x4140;" : "=r"(d) : "r"(mreg[e >> 1]), "r"(magic));
+    return u2h(d);
+  } else {
+    return unpack_elem<LANES>(ld_elem<LANES>(Mrow + j * LANES), magic);
+  }
+}
+
+template <int LANES, bool REGMSG>
+__device__ __forceinline__ void msg_store(uint8_t* Mrow, uint32_t* mreg, int j, int e, half2 biased,
+                                          bool st_ok) {
+  if constexpr (REGMSG) {
+    mreg[e >> 1] = __byte_perm(h2u(biased), mreg[e >> 1], (e & 1) ? 0x2054 : 0x7620);
+  } else {
+    st_elem_if<LANES>(Mrow + j * LANES, pack_elem<LANES>(biased), st_ok);
+  }
+}
+
 // One layer (base row r) for thread (group, z): gather, min-sum check-node
-// update, scatter. decoder.py:295-320. Messages are thread-major
-// (Mz = this thread's message row), so edge j of the row is at Mrow + j*LANES.
-template <int MAXW, int LANES>
-__device__ __forceinline__ void process_row(const KParams& p, const int e0, const int w, uint32_t zl,
-                                            uint32_t ZL, uint8_t* __restrict__ Lg,
-                                            uint8_t* __restrict__ Mz, const uint16_t* __restrict__ lut,
-                                            uint32_t magic, uint32_t one, bool st_ok) {
+// update, scatter. decoder.py:295-320. e0 indexes the graph tables; me0 is
+// the row's first edge in this thread's shared-memory message row.
+template <int MAXW, int LANES, bool REGMSG>
+__device__ __forceinline__ void process_row(const KParams& p, const int e0, const int me0, const int w,
+                                            uint32_t zl, uint32_t ZL, uint8_t* __restrict__ Lg,
+                                            uint8_t* __restrict__ Mz, uint32_t* mreg,
+                                            const uint16_t* __restrict__ lut, uint32_t magic,
+                                            uint32_t one, bool st_ok) {
   const half2 H127 = u2h(0x57F057F0u);   // 127.0
   const half2 H1152 = u2h(0x64806480u);  // 1152.0
-  uint8_t* Mrow = Mz + e0 * LANES;
+  uint8_t* Mrow = Mz + me0 * LANES;
   uint32_t off[MAXW];
   half2 t[MAXW];
   half2 m1 = H127, m2 = H127;
@@ -93,7 +122,7 @@ __device__ __forceinline__ void process_row(const KParams& p, const int e0, cons
     if (j < w) {
       off[j] = edge_offset(p, e0 + j, zl, ZL);
       const half2 lh = unpack_elem<LANES>(ld_elem<LANES>(Lg + off[j]), magic);
-      const half2 mh = unpack_elem<LANES>(ld_elem<LANES>(Mrow + j * LANES), magic);
+      const half2 mh = msg_load<LANES, REGMSG>(Mrow, mreg, j, j, magic);
       const half2 tj = __hsub2(lh, mh);           // exact: L - M
       const half2 aj = __habs2(tj);
       m2 = __hmin2(m2, __hmax2(m1, aj));          // kernels.py:247-250
@@ -102,23 +131,25 @@ __device__ __forceinline__ void process_row(const KParams& p, const int e0, cons
       t[j] = tj;
     }
   }
-  // beta-scaled magnitudes, with the row sign folded in: b' = (-1)^S * b
+  // beta-scaled magnitudes with the row sign folded in: b' = (-1)^S * b
   const half2 b1 = beta_lut2(lut, m1);
   const half2 b2 = beta_lut2(lut, m2);
   const half2 sig = u2h((S & 0x80008000u) | one);
-  const half2 d = __hmul2(__hsub2(b2, b1), sig);
-  const half2 b1s = __hmul2(b1, sig);
+  const half2 dd = __hmul2(__hsub2(b1, b2), sig);  // (b1 - b2)'
+  const half2 b2s = __hmul2(b2, sig);              // b2'
 #pragma unroll
   for (int j = 0; j < MAXW; ++j) {
     if (j < w) {
-      const half2 aj = __habs2(t[j]);
-      // edge holding the minimum gets m2 (a tie implies m1 == m2)
-      const half2 mag = __hfma2(__heq2(aj, m1), d, b1s);
-      // L' = sign(t) * min(|clamp t| + mag', 127)   == clamp127(t + out)
-      const half2 y = __hmin2(__hadd2(__hmin2(aj, H127), mag), H127);
+      // x = 0 for the edge holding the minimum (it gets m2; a tie implies
+      // m1 == m2), else 1: |t| - m1 is a non-negative integer, saturated.
+      const half2 x = __hsub2_sat(__habs2(t[j]), m1);
+      const half2 mag = __hfma2(x, dd, b2s);       // +-b1 or +-b2
+      // L' = sign(t) * min(|clamp t| + mag', 127) == clamp127(t + out), using
+      // min(|t|,127) + mag' = min(|t| + mag', 127 + mag')
+      const half2 y = __hmin2(__hmin2(__hadd2(__habs2(t[j]), mag), __hadd2(mag, H127)), H127);
       const half2 sg = u2h((h2u(t[j]) & 0x80008000u) | one);
       st_elem_if<LANES>(Lg + off[j], pack_elem<LANES>(__hfma2(y, sg, H1152)), st_ok);
-      st_elem_if<LANES>(Mrow + j * LANES, pack_elem<LANES>(__hfma2(mag, sg, H1152)), st_ok);
+      msg_store<LANES, REGMSG>(Mrow, mreg, j, j, __hfma2(mag, sg, H1152), st_ok);
     }
   }
 }
@@ -170,44 +201,123 @@ struct RowCtx {
   bool st_ok;
 };
 
-template <int BG, int MAXW, int LANES, int R>
-__device__ __forceinline__ void layers_ct(const KParams& p, const RowCtx& c) {
-  if constexpr (R < RowW<BG>::n) {
-    if (R < p.rows) {
-      constexpr int E0 = RowW<BG>::e0[R];
-      constexpr int W = RowW<BG>::w[R];
-      process_row<MAXW, LANES>(p, E0, W, c.zl, c.ZL, c.Lg, c.Mz, c.lut, c.magic,
-                               c.one, c.st_ok);
-      __syncthreads();
-      layers_ct<BG, MAXW, LANES, R + 1>(p, c);
-    }
+template <int N>
+struct IC {
+  static constexpr int value = N;
+};
+
+// Calls f(IC<W>{}) for the row weights that occur in the base graph, so each
+// layer body is compiled once per weight (not once per row): the whole
+// iteration stays within the instruction cache.
+// w == k through inline PTX, so LLVM cannot fold the chain below back into a
+// switch (jump table)
+__device__ __forceinline__ bool weq(int w, int k) {
+  int r;
+  asm("{ .reg .pred q; setp.eq.s32 q, %1, %2; selp.s32 %0, 1, 0, q; }" : "=r"(r) : "r"(w), "r"(k));
+  return r != 0;
+}
+
+template <int BG, typename F>
+__device__ __forceinline__ void dispatch_w(int w, F&& f) {
+  // an if-chain on a uniform value compiles to uniform branches (BRA.U);
+  // a switch becomes BRX on a vector register, which makes ptxas demote the
+  // row index and every graph-table load to per-thread registers
+  if constexpr (BG == 1) {
+    if (weq(w, 5)) f(IC<5>{});
+    else if (weq(w, 6)) f(IC<6>{});
+    else if (weq(w, 4)) f(IC<4>{});
+    else if (weq(w, 7)) f(IC<7>{});
+    else if (weq(w, 19)) f(IC<19>{});
+    else if (weq(w, 9)) f(IC<9>{});
+    else if (weq(w, 8)) f(IC<8>{});
+    else if (weq(w, 10)) f(IC<10>{});
+    else if (weq(w, 3)) f(IC<3>{});
+  } else {
+    if (weq(w, 4)) f(IC<4>{});
+    else if (weq(w, 5)) f(IC<5>{});
+    else if (weq(w, 3)) f(IC<3>{});
+    else if (weq(w, 6)) f(IC<6>{});
+    else if (weq(w, 8)) f(IC<8>{});
+    else if (weq(w, 10)) f(IC<10>{});
   }
 }
 
-template <int BG, int MAXW, int LANES, int R>
-__device__ __forceinline__ void parity_ct(const KParams& p, uint32_t zl, uint32_t ZL,
-                                          const uint8_t* __restrict__ Lg, int& wa, int& wb) {
-  if constexpr (R < RowW<BG>::n) {
-    if (R < p.rows) {
-      constexpr int E0 = RowW<BG>::e0[R];
-      constexpr int W = RowW<BG>::w[R];
-      row_parity<MAXW, LANES>(p, E0, W, zl, ZL, Lg, wa, wb);
-      parity_ct<BG, MAXW, LANES, R + 1>(p, zl, ZL, Lg, wa, wb);
+// Register-resident messages (BG1 pairs at the largest Z, see choose_shape):
+// the four 19-edge core rows keep their messages in a rotating queue of
+// 4 x 10 registers (the head is always the row being processed, so one loop
+// body serves all four rows); rows 4 and 5 (weights 3 and 8) use their own
+// registers when NREG == 6.
+template <int NREG>
+struct RegMsg {
+  static constexpr int nq = NREG >= 4 ? 4 : NREG;
+  uint32_t q[nq > 0 ? nq : 1][10];
+  uint32_t r4[2];
+  uint32_t r5[4];
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int k = 0; k < (nq > 0 ? nq : 1); ++k)
+#pragma unroll
+      for (int i = 0; i < 10; ++i) q[k][i] = 0x80808080u;  // zero messages (biased)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) r4[i] = 0x80808080u;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) r5[i] = 0x80808080u;
+  }
+  __device__ __forceinline__ void rotate() {
+    if constexpr (nq > 1) {
+      uint32_t h[10];
+#pragma unroll
+      for (int i = 0; i < 10; ++i) h[i] = q[0][i];
+#pragma unroll
+      for (int k = 0; k + 1 < nq; ++k)
+#pragma unroll
+        for (int i = 0; i < 10; ++i) q[k][i] = q[k + 1][i];
+#pragma unroll
+      for (int i = 0; i < 10; ++i) q[nq - 1][i] = h[i];
     }
   }
-}
+};
 
-template <int BG, int MAXW, int LANES>
-__device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c) {
+template <int BG, int MAXW, int LANES, int NREG>
+__device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c, RegMsg<NREG>& rm) {
   if constexpr (BG == 0) {
     for (int r = 0; r < p.rows; ++r) {
       const int e0 = p.row_start[r];
-      process_row<MAXW, LANES>(p, e0, p.row_start[r + 1] - e0, c.zl, c.ZL, c.Lg, c.Mz, c.lut, c.magic,
-                               c.one, c.st_ok);
+      process_row<MAXW, LANES, false>(p, e0, e0, p.row_start[r + 1] - e0, c.zl, c.ZL, c.Lg, c.Mz,
+                                      rm.r4, c.lut, c.magic, c.one, c.st_ok);
       __syncthreads();
     }
   } else {
-    layers_ct<BG, MAXW, LANES, 0>(p, c);
+    int r0 = 0;
+    if constexpr (NREG > 0) {
+#pragma unroll 1
+      for (int r = 0; r < RegMsg<NREG>::nq; ++r) {
+        process_row<19, LANES, true>(p, 19 * r, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, rm.q[0], c.lut, c.magic,
+                                     c.one, c.st_ok);
+        rm.rotate();
+        __syncthreads();
+      }
+      if constexpr (NREG == 6) {
+        process_row<3, LANES, true>(p, 76, 0, 3, c.zl, c.ZL, c.Lg, c.Mz, rm.r4, c.lut, c.magic, c.one,
+                                    c.st_ok);
+        __syncthreads();
+        process_row<8, LANES, true>(p, 79, 0, 8, c.zl, c.ZL, c.Lg, c.Mz, rm.r5, c.lut, c.magic, c.one,
+                                    c.st_ok);
+        __syncthreads();
+      }
+      r0 = NREG;
+    }
+#pragma unroll 1
+    for (int r = r0; r < p.rows; ++r) {
+      const int e0 = p.row_start[r];
+      const int w = p.row_start[r + 1] - e0;
+      dispatch_w<BG>(w, [&](auto W) {
+        process_row<decltype(W)::value, LANES, false>(p, e0, e0 - p.e_reg, decltype(W)::value, c.zl,
+                                                      c.ZL, c.Lg, c.Mz, rm.r4, c.lut, c.magic, c.one,
+                                                      c.st_ok);
+      });
+      __syncthreads();
+    }
   }
 }
 
@@ -221,7 +331,13 @@ __device__ __forceinline__ void local_check(const KParams& p, uint32_t zl, uint3
       row_parity<MAXW, LANES>(p, e0, p.row_start[r + 1] - e0, zl, ZL, Lg, wa, wb);
     }
   } else {
-    parity_ct<BG, MAXW, LANES, 0>(p, zl, ZL, Lg, wa, wb);
+#pragma unroll 1
+    for (int r = 0; r < p.rows; ++r) {
+      const int e0 = p.row_start[r];
+      dispatch_w<BG>(p.row_start[r + 1] - e0, [&](auto W) {
+        row_parity<decltype(W)::value, LANES>(p, e0, decltype(W)::value, zl, ZL, Lg, wa, wb);
+      });
+    }
   }
   int ma = 255, mb = 255;
   for (int c = 0; c < p.n_blocks; ++c) {
@@ -275,9 +391,10 @@ __device__ bool crc_ok_serial(const KParams& p, const uint8_t* __restrict__ Lg, 
 // Threads beyond G*Z (warp padding) shadow the last group's z = tid - (G-1)*Z
 // clamp but never store, so the layer loop runs warp-uniform and the graph
 // tables stay in uniform registers.
-template <int BG, int MAXW, int LANES>
-__global__ void __launch_bounds__(512) k_decode_i8(const __grid_constant__ KParams p,
-                                                   const int8_t* __restrict__ llr, KOut o) {
+template <int BG, int MAXW, int LANES, int NREG>
+__global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_constant__ KParams p,
+                                                                   const int8_t* __restrict__ llr, KOut o) {
+  static_assert(NREG == 0 || (BG == 1 && LANES == 2), "register messages: BG1 pairs only");
   extern __shared__ __align__(16) uint8_t smem[];
   uint16_t* lut = reinterpret_cast<uint16_t*>(smem);
   CtaState* cta = reinterpret_cast<CtaState*>(smem + kLutBytes);
@@ -336,7 +453,7 @@ __global__ void __launch_bounds__(512) k_decode_i8(const __grid_constant__ KPara
       }
       st_elem<LANES>(Lg + (uint32_t)n * LANES, v);
     }
-    for (int e = 0; e < p.n_edges; ++e) st_elem<LANES>(Mz + e * LANES, 0x8080u);
+    for (int e = 0; e < p.n_edges - p.e_reg; ++e) st_elem<LANES>(Mz + e * LANES, 0x8080u);
     if (bad && o.status) atomicOr(o.status, 1);
   }
   __syncthreads();
@@ -344,8 +461,10 @@ __global__ void __launch_bounds__(512) k_decode_i8(const __grid_constant__ KPara
   const uint32_t magic = p.magic;  // 0x64646464, opaque to ptxas
   const uint32_t one = p.one;      // 0x3C003C00 (half2 1.0)
   const RowCtx rc{zl, ZL, Lg, Mz, lut, magic, one, st_ok};
+  RegMsg<NREG> rm;
+  rm.init();
   for (int it = 1; it <= p.max_iter; ++it) {
-    one_iteration<BG, MAXW, LANES>(p, rc);
+    one_iteration<BG, MAXW, LANES, NREG>(p, rc, rm);
     const bool last = it == p.max_iter;
     if (!(p.early_stop != NRLDPC_STOP_NONE || p.trace || last)) continue;
 
@@ -505,6 +624,7 @@ struct nrldpc_plan {
   int k_b = 0, z = 0, rows = 0, n_blocks = 0, n_edges = 0, maxw = 0;
   int lanes = 1, groups = 1, threads = 32;
   int schedule = 0;  // 0 generic, 1/2: compile-time BG1/BG2 row schedule
+  int nreg = 0;      // leading rows whose messages live in registers (BG1 pairs)
   size_t smem = 0;
   KParams kp{};
   // host-path staging (nrldpc_decode_host)
@@ -532,12 +652,12 @@ size_t smem_for(int groups, size_t l_bytes, size_t m_bytes) {
   return kLutBytes + kCtaBytes + sizeof(GroupState) * groups + 16 + groups * (l_bytes + m_bytes);
 }
 
-template <int BG, int MAXW, int LANES>
+template <int BG, int MAXW, int LANES, int NREG = 0>
 cudaError_t launch_i8(const nrldpc_plan* plan, const int8_t* llr, long long batch, const KOut& o,
                       cudaStream_t st) {
   static bool attr_done[64] = {};
   const int dev = plan->device;
-  auto kern = k_decode_i8<BG, MAXW, LANES>;
+  auto kern = k_decode_i8<BG, MAXW, LANES, NREG>;
   if (!attr_done[dev & 63]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (e != cudaSuccess) return e;
@@ -569,25 +689,43 @@ uint16_t float_to_half_bits(float f) {
   return b;
 }
 
-// Pick lanes (codewords per half2) and groups per CTA. Smaller CTAs keep the
-// per-layer barrier cheap; more codewords per SM come from more CTAs.
+// Pick lanes (codewords per half2), register-resident message rows and
+// groups per CTA. Two codewords per lane (half2) whenever the pair's state
+// fits on chip; for BG1 at the largest Z the first rows' messages move from
+// shared memory into registers to make room. Smaller CTAs keep the per-layer
+// barrier cheap; more codewords per SM come from more CTAs.
 void choose_shape(nrldpc_plan* p) {
   const size_t smem_max = 232448;
   const size_t n_pos = (size_t)p->n_blocks * p->z;
-  int lanes = 2;
-  if (smem_for(1, align16(n_pos * 2), align16((size_t)p->z * padded_edges(p->n_edges, 2) * 2)) > smem_max)
-    lanes = 1;
+  auto msg_bytes = [&](int lanes, int e_reg) {
+    return align16((size_t)p->z * padded_edges(p->n_edges - e_reg, lanes) * lanes);
+  };
+  int lanes = 1, nreg = 0;
+  if (smem_for(1, align16(n_pos * 2), msg_bytes(2, 0)) <= smem_max) {
+    lanes = 2;
+  } else if (p->schedule == 1) {
+    for (int nr : {2, 4, 6}) {
+      if (nr > p->rows || p->z > 384) break;
+      if (smem_for(1, align16(n_pos * 2), msg_bytes(2, RowW<1>::e0[nr])) <= smem_max) {
+        lanes = 2;
+        nreg = nr;
+        break;
+      }
+    }
+  }
+  const int e_reg = nreg ? RowW<1>::e0[nreg] : 0;
   const size_t lb = align16(n_pos * lanes);
-  const size_t e_pad = padded_edges(p->n_edges, lanes);
-  const size_t mb = align16((size_t)p->z * e_pad * lanes);
+  const size_t e_pad = padded_edges(p->n_edges - e_reg, lanes);
+  const size_t mb = msg_bytes(lanes, e_reg);
   int best_g = 1;
   double best_waste = 1e9;
-  for (int g = 1; g * p->z <= 512; ++g) {
+  const int max_thr = nreg ? 384 : 512;
+  for (int g = 1; g * p->z <= max_thr; ++g) {
     if (smem_for(g, lb, mb) > smem_max) break;
     const int thr = g * p->z;
     const int thr32 = (thr + 31) / 32 * 32;
     const double waste = double(thr32 - thr) / thr32;
-    if (thr32 < 64 && (g + 1) * p->z <= 512 && smem_for(g + 1, lb, mb) <= smem_max) continue;
+    if (thr32 < 64 && (g + 1) * p->z <= max_thr && smem_for(g + 1, lb, mb) <= smem_max) continue;
     if (waste < best_waste - 1e-9) {
       best_waste = waste;
       best_g = g;
@@ -595,6 +733,7 @@ void choose_shape(nrldpc_plan* p) {
     if (waste <= 1.0 / 16) break;
   }
   p->lanes = lanes;
+  p->nreg = nreg;
   p->groups = best_g;
   p->threads = (best_g * p->z + 31) / 32 * 32;
   p->smem = smem_for(best_g, lb, mb);
@@ -602,6 +741,7 @@ void choose_shape(nrldpc_plan* p) {
   p->kp.l_bytes = (uint32_t)lb;
   p->kp.m_bytes = (uint32_t)mb;
   p->kp.m_stride = (uint32_t)(e_pad * lanes);
+  p->kp.e_reg = e_reg;
   p->kp.magic = 0x64646464u;
   p->kp.one = 0x3C003C00u;
   for (int e = 0; e < p->n_edges; ++e) {
@@ -724,7 +864,6 @@ int nrldpc_plan_create(int device, int k_b, int z, int rows_used, const int32_t*
   }
   // int8 beta rule: floor(beta * m) computed in float64 (decoder.py:208-212)
   for (int m = 0; m < 128; ++m) kp.lut[m] = float_to_half_bits((float)std::floor(beta * (double)m));
-  choose_shape(p);
   p->schedule = 0;
   for (int bg = 1; bg <= 2; ++bg) {
     const int kb_bg = bg == 1 ? 22 : 10;
@@ -735,6 +874,7 @@ int nrldpc_plan_create(int device, int k_b, int z, int rows_used, const int32_t*
       same = row_start[r] == (bg == 1 ? RowW<1>::e0[r] : RowW<2>::e0[r]);
     if (same) p->schedule = bg;
   }
+  choose_shape(p);
   *out = p;
   return NRLDPC_OK;
 }
@@ -812,7 +952,13 @@ static int decode_impl(const nrldpc_plan* plan, const void* llr, int64_t batch, 
     const int8_t* in = static_cast<const int8_t*>(llr);
     const bool two = plan->lanes == 2;
     switch (plan->schedule) {
-      case 1: e = two ? launch_i8<1, 19, 2>(plan, in, batch, o, st) : launch_i8<1, 19, 1>(plan, in, batch, o, st); break;
+      case 1:
+        if (!two) e = launch_i8<1, 19, 1>(plan, in, batch, o, st);
+        else if (plan->nreg == 0) e = launch_i8<1, 19, 2>(plan, in, batch, o, st);
+        else if (plan->nreg == 2) e = launch_i8<1, 19, 2, 2>(plan, in, batch, o, st);
+        else if (plan->nreg == 4) e = launch_i8<1, 19, 2, 4>(plan, in, batch, o, st);
+        else e = launch_i8<1, 19, 2, 6>(plan, in, batch, o, st);
+        break;
       case 2: e = two ? launch_i8<2, 10, 2>(plan, in, batch, o, st) : launch_i8<2, 10, 1>(plan, in, batch, o, st); break;
       default:
         if (plan->maxw > 10)
@@ -895,6 +1041,7 @@ int nrldpc_decode_host(nrldpc_plan* plan, const void* llr_host, int64_t batch, u
                             nb * per_cw_in, cudaMemcpyHostToDevice, st));
     KOut o{d_bits + b0 * words, d_iters + b0, d_synd + b0, d_succ + b0,
            crc_ok ? d_crc + b0 : nullptr, nullptr, nullptr, d_status};
+    g_launches = 0;
     const int rc = decode_impl(plan, d_llr + b0 * per_cw_in, nb, o, st);
     if (rc != NRLDPC_OK) return rc;
     launches += g_launches;

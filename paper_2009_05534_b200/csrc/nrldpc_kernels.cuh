@@ -49,6 +49,7 @@ struct KParams {
   uint32_t l_bytes;  // per group: n_blocks*z*LANES rounded up to 16
   uint32_t m_bytes;  // per group: z * m_stride rounded up to 16
   uint32_t m_stride; // bytes between consecutive z message rows (odd # words)
+  int e_reg;         // edges whose messages live in registers (rows < nreg)
   uint32_t magic;    // 0x64646464: PRMT filler byte (half exponent of 1024)
   uint32_t one;      // 0x3C003C00: half2 {1.0, 1.0}
   uint16_t row_start[NR_MAX_ROWS + 1];
