@@ -129,6 +129,13 @@ int nrldpc_decode_host(nrldpc_plan* plan, const void* llr_host, int64_t batch,
  */
 int nrldpc_alu_peak(int device, double* alu_lane_ops_per_s, double* mixed_lane_ops_per_s);
 
+/*
+ * The int8 beta rule floor(beta*m) (decoder.py:208-212) as exact half
+ * arithmetic: mode=1 when RN_half(beta_h*(m - delta) + c) - c equals it for
+ * every m in [0,127] (the kernel then skips its lookup table). Host only.
+ */
+int nrldpc_beta_rule(double beta, int* mode, float* beta_h, float* delta, float* c);
+
 /* Number of kernel launches the last nrldpc_decode/_quantize issued. */
 int nrldpc_launch_count(void);
 

@@ -33,6 +33,7 @@ EXPORTS = (
     "nrldpc_decode_host",
     "nrldpc_launch_count",
     "nrldpc_alu_peak",
+    "nrldpc_beta_rule",
     "nrldpc_last_error",
 )
 
@@ -75,6 +76,8 @@ def load() -> ctypes.CDLL:
     lib.nrldpc_decode_host.restype = c_int
     lib.nrldpc_alu_peak.argtypes = [c_int, c_void_p, c_void_p]
     lib.nrldpc_alu_peak.restype = c_int
+    lib.nrldpc_beta_rule.argtypes = [c_double, c_void_p, c_void_p, c_void_p, c_void_p]
+    lib.nrldpc_beta_rule.restype = c_int
     lib.nrldpc_launch_count.argtypes = []
     lib.nrldpc_launch_count.restype = c_int
     lib.nrldpc_last_error.argtypes = []

@@ -132,11 +132,22 @@ __device__ __forceinline__ void process_row(const KParams& p, const int e0, cons
     }
   }
   // beta-scaled magnitudes with the row sign folded in: b' = (-1)^S * b
-  const half2 b1 = beta_lut2(lut, m1);
-  const half2 b2 = beta_lut2(lut, m2);
   const half2 sig = u2h((S & 0x80008000u) | one);
-  const half2 dd = __hmul2(__hsub2(b1, b2), sig);  // (b1 - b2)'
-  const half2 b2s = __hmul2(b2, sig);              // b2'
+  half2 dd, b2s;  // (b1 - b2)' and b2'
+  if (p.beta_mode) {
+    // floor(beta*m) == RN(beta_h*(m - delta) + C) - C for every m in [0,127]
+    // (verified exhaustively on the host); all FMA-pipe, no table lookups
+    const half2 bh = u2h(p.beta_h), nd = u2h(p.ndelta_h), cc = u2h(p.c_h);
+    const half2 B1 = __hfma2(__hadd2(m1, nd), bh, cc);
+    const half2 B2 = __hfma2(__hadd2(m2, nd), bh, cc);
+    dd = __hmul2(__hsub2(B1, B2), sig);
+    b2s = __hmul2(__hsub2(B2, cc), sig);
+  } else {
+    const half2 b1 = beta_lut2(lut, m1);
+    const half2 b2 = beta_lut2(lut, m2);
+    dd = __hmul2(__hsub2(b1, b2), sig);
+    b2s = __hmul2(b2, sig);
+  }
 #pragma unroll
   for (int j = 0; j < MAXW; ++j) {
     if (j < w) {
@@ -689,6 +700,52 @@ uint16_t float_to_half_bits(float f) {
   return b;
 }
 
+// Half-precision arithmetic form of the int8 beta rule, if one exists:
+// floor(beta*m) == RN_half(bh*(m - delta) + C) - C for all m in [0,127], with
+// bh, delta, C halves and the FMA rounded once (HFMA2). Checked exhaustively
+// here, so the device never depends on an unverified identity; otherwise the
+// kernel falls back to the 128-entry LUT.
+double half_round(double x) {  // x in [1024, 2048): half ulp is 1
+  return std::nearbyint(x);
+}
+
+void find_beta_arith(double beta, KParams* kp) {
+  kp->beta_mode = 0;
+  const float bf = (float)beta;
+  const __half bh0 = __float2half_rn(bf);
+  uint16_t b0;
+  std::memcpy(&b0, &bh0, 2);
+  for (int db = 0; db <= 64; ++db) {
+    for (int sgn = 0; sgn < 2; ++sgn) {
+      const int bits = sgn ? (int)b0 - db : (int)b0 + db;
+      if (bits <= 0 || bits >= 0x3C01) continue;  // (0, 1]
+      __half hb;
+      const uint16_t ub = (uint16_t)bits;
+      std::memcpy(&hb, &ub, 2);
+      const double bh = (double)__half2float(hb);
+      for (int d16 = 0; d16 <= 16; ++d16) {
+        const double delta = d16 / 16.0;
+        for (int c = 1025; c <= 1040; ++c) {
+          bool ok = true;
+          for (int m = 0; m < 128 && ok; ++m) {
+            const double x = bh * ((double)m - delta) + (double)c;  // exact in double
+            if (x < 1024.0 || x >= 2048.0) { ok = false; break; }
+            ok = half_round(x) - c == std::floor(beta * (double)m);
+          }
+          if (ok) {
+            kp->beta_mode = 1;
+            kp->beta_h = (uint32_t)ub * 0x10001u;
+            kp->ndelta_h = (uint32_t)float_to_half_bits((float)-delta) * 0x10001u;
+            kp->c_h = (uint32_t)float_to_half_bits((float)c) * 0x10001u;
+            return;
+          }
+        }
+      }
+      if (db == 0) break;
+    }
+  }
+}
+
 // Pick lanes (codewords per half2), register-resident message rows and
 // groups per CTA. Two codewords per lane (half2) whenever the pair's state
 // fits on chip; for BG1 at the largest Z the first rows' messages move from
@@ -755,6 +812,25 @@ void choose_shape(nrldpc_plan* p) {
 extern "C" {
 
 const char* nrldpc_last_error(void) { return g_last_error.c_str(); }
+
+int nrldpc_beta_rule(double beta, int* mode, float* beta_h, float* delta, float* c) {
+  KParams kp{};
+  find_beta_arith(beta, &kp);
+  if (mode) *mode = kp.beta_mode;
+  if (kp.beta_mode) {
+    __half h;
+    uint16_t u = (uint16_t)(kp.beta_h & 0xFFFF);
+    std::memcpy(&h, &u, 2);
+    if (beta_h) *beta_h = __half2float(h);
+    u = (uint16_t)(kp.ndelta_h & 0xFFFF);
+    std::memcpy(&h, &u, 2);
+    if (delta) *delta = -__half2float(h);
+    u = (uint16_t)(kp.c_h & 0xFFFF);
+    std::memcpy(&h, &u, 2);
+    if (c) *c = __half2float(h);
+  }
+  return NRLDPC_OK;
+}
 
 int nrldpc_alu_peak(int device, double* alu_lane_ops_per_s, double* mixed_lane_ops_per_s) {
   NR_CUDA(cudaSetDevice(device));
@@ -864,6 +940,7 @@ int nrldpc_plan_create(int device, int k_b, int z, int rows_used, const int32_t*
   }
   // int8 beta rule: floor(beta * m) computed in float64 (decoder.py:208-212)
   for (int m = 0; m < 128; ++m) kp.lut[m] = float_to_half_bits((float)std::floor(beta * (double)m));
+  find_beta_arith(beta, &kp);
   p->schedule = 0;
   for (int bg = 1; bg <= 2; ++bg) {
     const int kb_bg = bg == 1 ? 22 : 10;

@@ -55,6 +55,8 @@ struct KParams {
   uint16_t row_start[NR_MAX_ROWS + 1];
   uint16_t shift_l[NR_MAX_EDGES];   // shift * LANES (bytes)
   uint32_t colbase[NR_MAX_EDGES];   // col * z * LANES (bytes)
+  int beta_mode;                    // 1: half-arithmetic beta (beta_h, ndelta_h, c_h)
+  uint32_t beta_h, ndelta_h, c_h;   // half2 constants of the arithmetic beta rule
   uint16_t lut[128];                // floor(beta*m) as half bits, m = 0..127
 };
 

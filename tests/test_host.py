@@ -178,3 +178,21 @@ def test_abi_rejects_bad_plans_without_gpu():
     rc = lib.nrldpc_plan_create(0, 22, 16, 4, rs.ctypes.data, cols.ctypes.data,
                                 sh.ctypes.data, 0, 1.5, 10, 0, 1, ctypes.byref(h))
     assert rc == _native.NRLDPC_EINVAL and b"beta" in lib.nrldpc_last_error()
+
+
+@pytest.mark.parametrize("beta", [0.75, 0.5, 1.0, 0.8, 0.3, 0.6875, 0.9, 0.123, 0.625])
+def test_beta_half_arithmetic_rule_is_exact(beta):
+    """The kernel's table-free beta rule, re-verified here with numpy halves."""
+    lib = _native.load()
+    mode, bh, delta, c = ctypes.c_int(), ctypes.c_float(), ctypes.c_float(), ctypes.c_float()
+    assert lib.nrldpc_beta_rule(beta, ctypes.byref(mode), ctypes.byref(bh), ctypes.byref(delta),
+                                ctypes.byref(c)) == 0
+    if beta in (0.75, 0.5, 1.0, 0.6875, 0.625):
+        assert mode.value == 1  # dyadic betas must take the fast path
+    if not mode.value:
+        return
+    m = np.arange(128, dtype=np.float64)
+    u = (m.astype(np.float16) - np.float16(delta.value)).astype(np.float16)   # HADD2, exact
+    fma = u.astype(np.float64) * np.float64(np.float16(bh.value)) + c.value  # exact product+sum
+    rounded = fma.astype(np.float16).astype(np.float64)                      # one rounding
+    assert np.array_equal(rounded - c.value, np.floor(beta * m))
