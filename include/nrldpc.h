@@ -90,7 +90,9 @@ int nrldpc_quantize(const nrldpc_plan* plan, const void* llr_in, int in_dtype,
 
 /*
  * Layered min-sum decode (decoder.py:486-566). All pointers are device
- * pointers; asynchronous on `stream`.
+ * pointers; asynchronous on `stream`. The plan caches per-device launch
+ * data (occupancy) on first use; decode calls on one plan from several host
+ * threads are safe once it has been used once.
  *   llr      : (batch, n_c) int8 | half | float per the plan's precision
  *   bits     : (batch, words) uint32, hard decisions of the first K
  *              positions, LSB-first (bit i of word w is position 32w+i)
@@ -105,7 +107,7 @@ int nrldpc_quantize(const nrldpc_plan* plan, const void* llr_in, int in_dtype,
  *   status   : (1,) int32 device word, set nonzero if an int8 input had
  *              magnitude > 127 (decoder.py:287-288); may be NULL.
  */
-int nrldpc_decode(const nrldpc_plan* plan, const void* llr, int64_t batch,
+int nrldpc_decode(nrldpc_plan* plan, const void* llr, int64_t batch,
                   uint32_t* bits, int32_t* iters, int32_t* synd,
                   uint8_t* success, uint8_t* crc_ok, int32_t* trace_w,
                   float* trace_m, int32_t* status, void* stream);

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -67,10 +68,32 @@ constexpr int kLutBytes = 256;
 constexpr int kCtaBytes = 16;
 
 // (z + s) mod Z for one edge, as a byte offset into the group's L array.
-__device__ __forceinline__ uint32_t edge_offset(const KParams& p, int e, uint32_t zl, uint32_t ZL) {
-  uint32_t a = zl + p.shift_l[e];
+__device__ __forceinline__ uint32_t edge_offset(uint32_t shift, uint32_t colbase, uint32_t zl, uint32_t ZL) {
+  uint32_t a = zl + shift;
   a = min(a, a - ZL);  // unsigned: picks a-ZL only when a >= ZL  (one VIADDMNMX)
-  return a + p.colbase[e];
+  return a + colbase;
+}
+
+// A row's shift/column tables (t0 is 4-aligned): 128-bit uniform loads.
+template <int MAXW>
+__device__ __forceinline__ void load_row_tables(const KParams& p, int t0, int w, uint32_t (&sh)[MAXW],
+                                                uint32_t (&cb)[MAXW]) {
+  const uint4* S = reinterpret_cast<const uint4*>(p.sh) + (t0 >> 2);
+  const uint4* C = reinterpret_cast<const uint4*>(p.cb) + (t0 >> 2);
+#pragma unroll
+  for (int k = 0; k < (MAXW + 3) / 4; ++k) {
+    if (4 * k < w) {
+      const uint4 a = S[k], b = C[k];
+      const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (4 * k + i < MAXW) {
+          sh[4 * k + i] = av[i];
+          cb[4 * k + i] = bv[i];
+        }
+      }
+    }
+  }
 }
 
 // Message access for one edge. Shared memory: thread-major rows (Mrow =
@@ -102,10 +125,11 @@ __device__ __forceinline__ void msg_store(uint8_t* Mrow, uint32_t* mreg, int j, 
 }
 
 // One layer (base row r) for thread (group, z): gather, min-sum check-node
-// update, scatter. decoder.py:295-320. e0 indexes the graph tables; me0 is
-// the row's first edge in this thread's shared-memory message row.
+// update, scatter. decoder.py:295-320. t0 is the row's slot in the graph
+// tables; me0 is the row's first edge in this thread's shared-memory message
+// row.
 template <int MAXW, int LANES, bool REGMSG>
-__device__ __forceinline__ void process_row(const KParams& p, const int e0, const int me0, const int w,
+__device__ __forceinline__ void process_row(const KParams& p, const int t0, const int me0, const int w,
                                             uint32_t zl, uint32_t ZL, uint8_t* __restrict__ Lg,
                                             uint8_t* __restrict__ Mz, uint32_t* mreg,
                                             const uint16_t* __restrict__ lut, uint32_t magic,
@@ -113,14 +137,15 @@ __device__ __forceinline__ void process_row(const KParams& p, const int e0, cons
   const half2 H127 = u2h(0x57F057F0u);   // 127.0
   const half2 H1152 = u2h(0x64806480u);  // 1152.0
   uint8_t* Mrow = Mz + me0 * LANES;
-  uint32_t off[MAXW];
+  uint32_t off[MAXW], tsh[MAXW], tcb[MAXW];
+  load_row_tables<MAXW>(p, t0, w, tsh, tcb);
   half2 t[MAXW];
   half2 m1 = H127, m2 = H127;
   uint32_t S = 0;
 #pragma unroll
   for (int j = 0; j < MAXW; ++j) {
     if (j < w) {
-      off[j] = edge_offset(p, e0 + j, zl, ZL);
+      off[j] = edge_offset(tsh[j], tcb[j], zl, ZL);
       const half2 lh = unpack_elem<LANES>(ld_elem<LANES>(Lg + off[j]), magic);
       const half2 mh = msg_load<LANES, REGMSG>(Mrow, mreg, j, j, magic);
       const half2 tj = __hsub2(lh, mh);           // exact: L - M
@@ -168,13 +193,15 @@ __device__ __forceinline__ void process_row(const KParams& p, const int e0, cons
 // Syndrome weight (decoder.py:323-329) and min|L| (decoder.py:480-483) over
 // the thread's check rows / columns.
 template <int MAXW, int LANES>
-__device__ __forceinline__ void row_parity(const KParams& p, const int e0, const int w, uint32_t zl,
+__device__ __forceinline__ void row_parity(const KParams& p, const int t0, const int w, uint32_t zl,
                                            uint32_t ZL, const uint8_t* __restrict__ Lg, int& wa,
                                            int& wb) {
+  uint32_t tsh[MAXW], tcb[MAXW];
+  load_row_tables<MAXW>(p, t0, w, tsh, tcb);
   uint32_t x = 0;
 #pragma unroll
   for (int j = 0; j < MAXW; ++j) {
-    if (j < w) x ^= ld_elem<LANES>(Lg + edge_offset(p, e0 + j, zl, ZL));
+    if (j < w) x ^= ld_elem<LANES>(Lg + edge_offset(tsh[j], tcb[j], zl, ZL));
   }
   // bit 7 of a stored byte is 1 for a non-negative value
   if (w & 1) x ^= 0x8080u;
@@ -274,6 +301,20 @@ struct RegMsg {
 #pragma unroll
     for (int i = 0; i < 4; ++i) r5[i] = 0x80808080u;
   }
+  // rows come in twos: after rows (2k, 2k+1) swap the head pair with the
+  // tail pair (nq == 4); nq == 2 needs no movement at all
+  __device__ __forceinline__ void rotate2() {
+    if constexpr (nq == 4) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int i = 0; i < 10; ++i) {
+          const uint32_t h = q[k][i];
+          q[k][i] = q[k + 2][i];
+          q[k + 2][i] = h;
+        }
+    }
+  }
   __device__ __forceinline__ void rotate() {
     if constexpr (nq > 1) {
       uint32_t h[10];
@@ -294,40 +335,50 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
   if constexpr (BG == 0) {
     for (int r = 0; r < p.rows; ++r) {
       const int e0 = p.row_start[r];
-      process_row<MAXW, LANES, false>(p, e0, e0, p.row_start[r + 1] - e0, c.zl, c.ZL, c.Lg, c.Mz,
+      process_row<MAXW, LANES, false>(p, p.tab_start[r], e0, p.row_start[r + 1] - e0, c.zl, c.ZL, c.Lg, c.Mz,
                                       rm.r4, c.lut, c.magic, c.one, c.st_ok);
-      __syncthreads();
+      if (p.bar_after[r]) __syncthreads();
     }
   } else {
     int r0 = 0;
     if constexpr (NREG > 0) {
 #pragma unroll 1
-      for (int r = 0; r < RegMsg<NREG>::nq; ++r) {
-        process_row<19, LANES, true>(p, 19 * r, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, rm.q[0], c.lut, c.magic,
+      for (int r = 0; r < RegMsg<NREG>::nq; r += 2) {
+        process_row<19, LANES, true>(p, 20 * r, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, rm.q[0], c.lut, c.magic,
                                      c.one, c.st_ok);
-        rm.rotate();
+        __syncthreads();
+        process_row<19, LANES, true>(p, 20 * r + 20, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, rm.q[1], c.lut,
+                                     c.magic, c.one, c.st_ok);
+        rm.rotate2();
         __syncthreads();
       }
       if constexpr (NREG == 6) {
-        process_row<3, LANES, true>(p, 76, 0, 3, c.zl, c.ZL, c.Lg, c.Mz, rm.r4, c.lut, c.magic, c.one,
+        process_row<3, LANES, true>(p, 80, 0, 3, c.zl, c.ZL, c.Lg, c.Mz, rm.r4, c.lut, c.magic, c.one,
                                     c.st_ok);
         __syncthreads();
-        process_row<8, LANES, true>(p, 79, 0, 8, c.zl, c.ZL, c.Lg, c.Mz, rm.r5, c.lut, c.magic, c.one,
+        process_row<8, LANES, true>(p, 84, 0, 8, c.zl, c.ZL, c.Lg, c.Mz, rm.r5, c.lut, c.magic, c.one,
                                     c.st_ok);
         __syncthreads();
       }
       r0 = NREG;
     }
+    // row descriptors are loaded one row ahead so the dispatch for the next
+    // row does not wait on the constant cache after the barrier
+    uint2 nd = p.rowdesc[r0];
 #pragma unroll 1
     for (int r = r0; r < p.rows; ++r) {
-      const int e0 = p.row_start[r];
-      const int w = p.row_start[r + 1] - e0;
+      const uint2 d = nd;
+      nd = p.rowdesc[r + 1];
+      const int t0 = (int)(d.x & 0xFFFFu);
+      const int w = (int)(d.x >> 16);
+      const int me0 = (int)(d.y & 0xFFFFu);
       dispatch_w<BG>(w, [&](auto W) {
-        process_row<decltype(W)::value, LANES, false>(p, e0, e0 - p.e_reg, decltype(W)::value, c.zl,
-                                                      c.ZL, c.Lg, c.Mz, rm.r4, c.lut, c.magic, c.one,
-                                                      c.st_ok);
+        process_row<decltype(W)::value, LANES, false>(p, t0, me0, decltype(W)::value, c.zl, c.ZL, c.Lg,
+                                                      c.Mz, rm.r4, c.lut, c.magic, c.one, c.st_ok);
       });
-      __syncthreads();
+      // consecutive column-disjoint rows form one layer: the next row reads
+      // no column this one wrote, so warps may run ahead into it
+      if (d.y >> 16) __syncthreads();
     }
   }
 }
@@ -339,14 +390,15 @@ __device__ __forceinline__ void local_check(const KParams& p, uint32_t zl, uint3
   if constexpr (BG == 0) {
     for (int r = 0; r < p.rows; ++r) {
       const int e0 = p.row_start[r];
-      row_parity<MAXW, LANES>(p, e0, p.row_start[r + 1] - e0, zl, ZL, Lg, wa, wb);
+      row_parity<MAXW, LANES>(p, p.tab_start[r], p.row_start[r + 1] - e0, zl, ZL, Lg, wa, wb);
     }
   } else {
 #pragma unroll 1
     for (int r = 0; r < p.rows; ++r) {
       const int e0 = p.row_start[r];
+      const int t0 = p.tab_start[r];
       dispatch_w<BG>(p.row_start[r + 1] - e0, [&](auto W) {
-        row_parity<decltype(W)::value, LANES>(p, e0, decltype(W)::value, zl, ZL, Lg, wa, wb);
+        row_parity<decltype(W)::value, LANES>(p, t0, decltype(W)::value, zl, ZL, Lg, wa, wb);
       });
     }
   }
@@ -446,25 +498,59 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
   lane_valid[0] = active;
   lane_valid[1] = active && LANES == 2 && cw0 + 1 < p.batch;
 
-  // load: int8 -> biased byte (x ^ 0x80), lanes interleaved; messages = 0
+  // load: int8 -> biased byte (x ^ 0x80), lanes interleaved; messages = 0.
+  // The group's Z threads cooperate; with 16-byte aligned rows each thread
+  // moves 16 positions per step (LDG.128 per codeword, PRMT interleave,
+  // STS.128), otherwise one position per thread per step.
   if (st_ok) {
-    int bad = 0;
-    for (int c = 0; c < p.n_blocks; ++c) {
-      const long long n = (long long)c * p.z + z;
-      uint32_t v = 0;
-#pragma unroll
-      for (int l = 0; l < LANES; ++l) {
-        uint32_t u = 0x80u;
-        if (lane_valid[l]) {
-          const int8_t x = llr[(cw0 + l) * n_c + n];
-          bad |= (x == -128);
-          u = (uint32_t)(uint8_t)x ^ 0x80u;
+    uint32_t bad = 0;
+    const uint4 zero4 = make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);
+    if (p.vec_load) {
+      const int chunks = (int)(n_c >> 4);
+      const uint4* rowA = reinterpret_cast<const uint4*>(llr + cw0 * n_c);
+      const uint4* rowB = reinterpret_cast<const uint4*>(llr + (cw0 + 1) * n_c);
+      for (int k = z; k < chunks; k += p.z) {
+        uint4 a = lane_valid[0] ? rowA[k] : make_uint4(0, 0, 0, 0);
+        a.x ^= 0x80808080u; a.y ^= 0x80808080u; a.z ^= 0x80808080u; a.w ^= 0x80808080u;
+        bad |= (a.x - 0x01010101u) & ~a.x; bad |= (a.y - 0x01010101u) & ~a.y;
+        bad |= (a.z - 0x01010101u) & ~a.z; bad |= (a.w - 0x01010101u) & ~a.w;
+        if (LANES == 2) {
+          uint4 b = lane_valid[1] ? rowB[k] : make_uint4(0, 0, 0, 0);
+          b.x ^= 0x80808080u; b.y ^= 0x80808080u; b.z ^= 0x80808080u; b.w ^= 0x80808080u;
+          if (lane_valid[1]) {
+            bad |= (b.x - 0x01010101u) & ~b.x; bad |= (b.y - 0x01010101u) & ~b.y;
+            bad |= (b.z - 0x01010101u) & ~b.z; bad |= (b.w - 0x01010101u) & ~b.w;
+          }
+          uint4* dst = reinterpret_cast<uint4*>(Lg) + 2 * k;
+          dst[0] = make_uint4(__byte_perm(a.x, b.x, 0x5140), __byte_perm(a.x, b.x, 0x7362),
+                              __byte_perm(a.y, b.y, 0x5140), __byte_perm(a.y, b.y, 0x7362));
+          dst[1] = make_uint4(__byte_perm(a.z, b.z, 0x5140), __byte_perm(a.z, b.z, 0x7362),
+                              __byte_perm(a.w, b.w, 0x5140), __byte_perm(a.w, b.w, 0x7362));
+        } else {
+          reinterpret_cast<uint4*>(Lg)[k] = a;
         }
-        v |= u << (8 * l);
       }
-      st_elem<LANES>(Lg + (uint32_t)n * LANES, v);
+      bad &= 0x80808080u;
+    } else {
+      for (int c = 0; c < p.n_blocks; ++c) {
+        const long long n = (long long)c * p.z + z;
+        uint32_t v = 0;
+#pragma unroll
+        for (int l = 0; l < LANES; ++l) {
+          uint32_t u = 0x80u;
+          if (lane_valid[l]) {
+            const int8_t x = llr[(cw0 + l) * n_c + n];
+            bad |= (x == -128);
+            u = (uint32_t)(uint8_t)x ^ 0x80u;
+          }
+          v |= u << (8 * l);
+        }
+        st_elem<LANES>(Lg + (uint32_t)n * LANES, v);
+      }
     }
-    for (int e = 0; e < p.n_edges - p.e_reg; ++e) st_elem<LANES>(Mz + e * LANES, 0x8080u);
+    // messages: the group's whole message area is contiguous (m_bytes % 16 == 0)
+    uint4* m4 = reinterpret_cast<uint4*>(Lg + p.l_bytes);
+    for (uint32_t k = z; k < (p.m_bytes >> 4); k += p.z) m4[k] = zero4;
     if (bad && o.status) atomicOr(o.status, 1);
   }
   __syncthreads();
@@ -625,6 +711,17 @@ __global__ void __launch_bounds__(512) k_alu_peak(uint32_t* out, int iters, uint
 // ---------------------------------------------------------------------------
 // Host side
 
+// One launch configuration of the decode kernel.
+struct Shape {
+  int lanes = 1;    // codewords per half2 lane pair
+  int nreg = 0;     // leading rows whose messages live in registers (BG1 pairs)
+  int groups = 1;   // codeword groups (of Z threads) per CTA
+  int threads = 32;
+  size_t smem = 0;
+  int occ = 0;      // resident CTAs per SM (0: not queried yet)
+  KParams kp{};
+};
+
 struct nrldpc_plan {
   int device = 0;
   int precision = NRLDPC_INT8;
@@ -633,11 +730,9 @@ struct nrldpc_plan {
   double beta = 0.75;
   int max_iter = 20;
   int k_b = 0, z = 0, rows = 0, n_blocks = 0, n_edges = 0, maxw = 0;
-  int lanes = 1, groups = 1, threads = 32;
   int schedule = 0;  // 0 generic, 1/2: compile-time BG1/BG2 row schedule
-  int nreg = 0;      // leading rows whose messages live in registers (BG1 pairs)
-  size_t smem = 0;
-  KParams kp{};
+  KParams base{};    // graph tables + config, before the shape-dependent scaling
+  Shape main;        // the launch shape
   // host-path staging (nrldpc_decode_host)
   std::mutex host_mu;
   cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
@@ -663,23 +758,32 @@ size_t smem_for(int groups, size_t l_bytes, size_t m_bytes) {
   return kLutBytes + kCtaBytes + sizeof(GroupState) * groups + 16 + groups * (l_bytes + m_bytes);
 }
 
+// Launch (or, with llr == nullptr, only prepare: set the smem attribute and
+// query occupancy) one decode kernel instance for `sh`.
 template <int BG, int MAXW, int LANES, int NREG = 0>
-cudaError_t launch_i8(const nrldpc_plan* plan, const int8_t* llr, long long batch, const KOut& o,
+cudaError_t launch_i8(Shape& sh, int device, const int8_t* llr, long long batch, const KOut& o,
                       cudaStream_t st) {
   static bool attr_done[64] = {};
-  const int dev = plan->device;
   auto kern = k_decode_i8<BG, MAXW, LANES, NREG>;
-  if (!attr_done[dev & 63]) {
+  if (!attr_done[device & 63]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (e != cudaSuccess) return e;
-    attr_done[dev & 63] = true;
+    attr_done[device & 63] = true;
   }
-  KParams kp = plan->kp;
+  if (!sh.occ) {
+    int occ = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, sh.threads, sh.smem);
+    if (e != cudaSuccess) return e;
+    sh.occ = occ > 0 ? occ : 1;
+  }
+  if (!llr) return cudaSuccess;
+  KParams kp = sh.kp;
   kp.batch = batch;
   kp.trace = o.trace_w != nullptr;
-  const long long per_cta = (long long)plan->groups * LANES;
+  kp.vec_load = ((long long)kp.n_blocks * kp.z) % 16 == 0 && ((uintptr_t)llr & 15) == 0;
+  const long long per_cta = (long long)sh.groups * LANES;
   const long long grid = (batch + per_cta - 1) / per_cta;
-  kern<<<(unsigned)grid, plan->threads, plan->smem, st>>>(kp, llr, o);
+  kern<<<(unsigned)grid, sh.threads, sh.smem, st>>>(kp, llr, o);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -751,22 +855,24 @@ void find_beta_arith(double beta, KParams* kp) {
 // fits on chip; for BG1 at the largest Z the first rows' messages move from
 // shared memory into registers to make room. Smaller CTAs keep the per-layer
 // barrier cheap; more codewords per SM come from more CTAs.
-void choose_shape(nrldpc_plan* p) {
+Shape choose_shape(const nrldpc_plan* p, int max_lanes) {
   const size_t smem_max = 232448;
   const size_t n_pos = (size_t)p->n_blocks * p->z;
   auto msg_bytes = [&](int lanes, int e_reg) {
     return align16((size_t)p->z * padded_edges(p->n_edges - e_reg, lanes) * lanes);
   };
   int lanes = 1, nreg = 0;
-  if (smem_for(1, align16(n_pos * 2), msg_bytes(2, 0)) <= smem_max) {
-    lanes = 2;
-  } else if (p->schedule == 1) {
-    for (int nr : {2, 4, 6}) {
-      if (nr > p->rows || p->z > 384) break;
-      if (smem_for(1, align16(n_pos * 2), msg_bytes(2, RowW<1>::e0[nr])) <= smem_max) {
-        lanes = 2;
-        nreg = nr;
-        break;
+  if (max_lanes >= 2) {
+    if (smem_for(1, align16(n_pos * 2), msg_bytes(2, 0)) <= smem_max) {
+      lanes = 2;
+    } else if (p->schedule == 1) {
+      for (int nr : {2, 4, 6}) {
+        if (nr > p->rows || p->z > 384) break;
+        if (smem_for(1, align16(n_pos * 2), msg_bytes(2, RowW<1>::e0[nr])) <= smem_max) {
+          lanes = 2;
+          nreg = nr;
+          break;
+        }
       }
     }
   }
@@ -789,25 +895,54 @@ void choose_shape(nrldpc_plan* p) {
     }
     if (waste <= 1.0 / 16) break;
   }
-  p->lanes = lanes;
-  p->nreg = nreg;
-  p->groups = best_g;
-  p->threads = (best_g * p->z + 31) / 32 * 32;
-  p->smem = smem_for(best_g, lb, mb);
-  p->kp.groups = best_g;
-  p->kp.l_bytes = (uint32_t)lb;
-  p->kp.m_bytes = (uint32_t)mb;
-  p->kp.m_stride = (uint32_t)(e_pad * lanes);
-  p->kp.e_reg = e_reg;
-  p->kp.magic = 0x64646464u;
-  p->kp.one = 0x3C003C00u;
-  for (int e = 0; e < p->n_edges; ++e) {
-    p->kp.shift_l[e] = (uint16_t)(p->kp.shift_l[e] * lanes);
-    p->kp.colbase[e] = p->kp.colbase[e] * (uint32_t)p->z * lanes;
+  Shape sh;
+  sh.lanes = lanes;
+  sh.nreg = nreg;
+  sh.groups = best_g;
+  sh.threads = (best_g * p->z + 31) / 32 * 32;
+  sh.smem = smem_for(best_g, lb, mb);
+  sh.kp = p->base;
+  sh.kp.groups = best_g;
+  sh.kp.l_bytes = (uint32_t)lb;
+  sh.kp.m_bytes = (uint32_t)mb;
+  sh.kp.m_stride = (uint32_t)(e_pad * lanes);
+  sh.kp.e_reg = e_reg;
+  for (int r = 0; r < p->rows; ++r) {
+    const int e0 = p->base.row_start[r];
+    const int w = p->base.row_start[r + 1] - e0;
+    sh.kp.rowdesc[r] = make_uint2((uint32_t)p->base.tab_start[r] | ((uint32_t)w << 16),
+                                  (uint32_t)(e0 - e_reg) | ((uint32_t)p->base.bar_after[r] << 16));
   }
+  sh.kp.magic = 0x64646464u;
+  sh.kp.one = 0x3C003C00u;
+  for (int t = 0; t < NR_MAX_TAB; ++t) {
+    sh.kp.sh[t] = p->base.sh[t] * lanes;
+    sh.kp.cb[t] = p->base.cb[t] * (uint32_t)p->z * lanes;
+  }
+  return sh;
 }
 
 }  // namespace
+
+static cudaError_t launch_shape(const nrldpc_plan* plan, Shape& sh, const int8_t* in, int64_t batch,
+                                const KOut& o, cudaStream_t st) {
+  const bool two = sh.lanes == 2;
+  const int dev = plan->device;
+  switch (plan->schedule) {
+    case 1:
+      if (!two) return launch_i8<1, 19, 1>(sh, dev, in, batch, o, st);
+      if (sh.nreg == 0) return launch_i8<1, 19, 2>(sh, dev, in, batch, o, st);
+      if (sh.nreg == 2) return launch_i8<1, 19, 2, 2>(sh, dev, in, batch, o, st);
+      if (sh.nreg == 4) return launch_i8<1, 19, 2, 4>(sh, dev, in, batch, o, st);
+      return launch_i8<1, 19, 2, 6>(sh, dev, in, batch, o, st);
+    case 2:
+      return two ? launch_i8<2, 10, 2>(sh, dev, in, batch, o, st) : launch_i8<2, 10, 1>(sh, dev, in, batch, o, st);
+    default:
+      if (plan->maxw > 10)
+        return two ? launch_i8<0, 19, 2>(sh, dev, in, batch, o, st) : launch_i8<0, 19, 1>(sh, dev, in, batch, o, st);
+      return two ? launch_i8<0, 10, 2>(sh, dev, in, batch, o, st) : launch_i8<0, 10, 1>(sh, dev, in, batch, o, st);
+  }
+}
 
 extern "C" {
 
@@ -921,7 +1056,7 @@ int nrldpc_plan_create(int device, int k_b, int z, int rows_used, const int32_t*
   p->n_blocks = n_blocks;
   p->n_edges = n_edges;
   p->maxw = maxw;
-  KParams& kp = p->kp;
+  KParams& kp = p->base;
   std::memset(&kp, 0, sizeof(kp));
   kp.z = z;
   kp.k_b = k_b;
@@ -934,9 +1069,32 @@ int nrldpc_plan_create(int device, int k_b, int z, int rows_used, const int32_t*
   kp.crc_poly = crc_poly;
   kp.words = (k_b * z + 31) / 32;
   for (int r = 0; r <= rows_used; ++r) kp.row_start[r] = (uint16_t)row_start[r];
-  for (int e = 0; e < n_edges; ++e) {
-    kp.shift_l[e] = (uint16_t)shifts[e];
-    kp.colbase[e] = (uint32_t)cols[e];
+  {
+    int t = 0;
+    for (int r = 0; r < rows_used; ++r) {
+      kp.tab_start[r] = (uint16_t)t;
+      for (int e = row_start[r]; e < row_start[r + 1]; ++e, ++t) {
+        kp.sh[t] = (uint32_t)shifts[e];
+        kp.cb[t] = (uint32_t)cols[e];
+      }
+      t = (t + 3) & ~3;
+    }
+    kp.tab_start[rows_used] = (uint16_t)t;
+  }
+  // layers: a barrier after row r unless row r+1 shares no column with any
+  // row since the last barrier (then r+1 can run concurrently with them).
+  // Rows 0..5 keep their barriers (register-message rows are straight-line).
+  {
+    uint64_t layer_cols = 0;
+    for (int r = 0; r < rows_used; ++r) {
+      for (int e = row_start[r]; e < row_start[r + 1]; ++e) layer_cols |= 1ull << cols[e];
+      uint64_t next = 0;
+      if (r + 1 < rows_used)
+        for (int e = row_start[r + 1]; e < row_start[r + 2]; ++e) next |= 1ull << cols[e];
+      const bool disjoint = r + 1 < rows_used && r >= 6 && (next & layer_cols) == 0;
+      kp.bar_after[r] = disjoint ? 0 : 1;
+      if (!disjoint) layer_cols = 0;
+    }
   }
   // int8 beta rule: floor(beta * m) computed in float64 (decoder.py:208-212)
   for (int m = 0; m < 128; ++m) kp.lut[m] = float_to_half_bits((float)std::floor(beta * (double)m));
@@ -951,7 +1109,22 @@ int nrldpc_plan_create(int device, int k_b, int z, int rows_used, const int32_t*
       same = row_start[r] == (bg == 1 ? RowW<1>::e0[r] : RowW<2>::e0[r]);
     if (same) p->schedule = bg;
   }
-  choose_shape(p);
+  const char* force = std::getenv("NRLDPC_FORCE_LANES");
+  p->main = choose_shape(p, force && force[0] == '1' ? 1 : 2);
+  // set kernel attributes and cache occupancy now, so decode never mutates
+  // the plan (concurrent decodes on one plan are then race-free)
+  {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    KOut none{};
+    const cudaError_t e1 = launch_shape(p, p->main, nullptr, 0, none, nullptr);
+    cudaSetDevice(prev);
+    if (e1 != cudaSuccess) {
+      delete p;
+      return cuda_fail(e1, "kernel setup");
+    }
+  }
   *out = p;
   return NRLDPC_OK;
 }
@@ -976,11 +1149,11 @@ int nrldpc_plan_info(const nrldpc_plan* plan, int64_t* k, int64_t* n_c, int64_t*
   if (k) *k = (int64_t)plan->k_b * plan->z;
   if (n_c) *n_c = (int64_t)plan->n_blocks * plan->z;
   if (n_tx) *n_tx = (int64_t)(plan->n_blocks - 2) * plan->z;
-  if (words_per_cw) *words_per_cw = plan->kp.words;
-  if (lanes) *lanes = plan->lanes;
-  if (groups_per_cta) *groups_per_cta = plan->groups;
-  if (threads_per_cta) *threads_per_cta = plan->threads;
-  if (smem_bytes) *smem_bytes = (int64_t)plan->smem;
+  if (words_per_cw) *words_per_cw = plan->base.words;
+  if (lanes) *lanes = plan->main.lanes;
+  if (groups_per_cta) *groups_per_cta = plan->main.groups;
+  if (threads_per_cta) *threads_per_cta = plan->main.threads;
+  if (smem_bytes) *smem_bytes = (int64_t)plan->main.smem;
   return NRLDPC_OK;
 }
 
@@ -1022,35 +1195,15 @@ int nrldpc_quantize(const nrldpc_plan* plan, const void* llr_in, int in_dtype, i
   return NRLDPC_OK;
 }
 
-static int decode_impl(const nrldpc_plan* plan, const void* llr, int64_t batch, const KOut& o,
+static int decode_impl(nrldpc_plan* plan, const void* llr, int64_t batch, const KOut& o,
                        cudaStream_t st) {
-  cudaError_t e = cudaSuccess;
-  if (plan->precision == NRLDPC_INT8) {
-    const int8_t* in = static_cast<const int8_t*>(llr);
-    const bool two = plan->lanes == 2;
-    switch (plan->schedule) {
-      case 1:
-        if (!two) e = launch_i8<1, 19, 1>(plan, in, batch, o, st);
-        else if (plan->nreg == 0) e = launch_i8<1, 19, 2>(plan, in, batch, o, st);
-        else if (plan->nreg == 2) e = launch_i8<1, 19, 2, 2>(plan, in, batch, o, st);
-        else if (plan->nreg == 4) e = launch_i8<1, 19, 2, 4>(plan, in, batch, o, st);
-        else e = launch_i8<1, 19, 2, 6>(plan, in, batch, o, st);
-        break;
-      case 2: e = two ? launch_i8<2, 10, 2>(plan, in, batch, o, st) : launch_i8<2, 10, 1>(plan, in, batch, o, st); break;
-      default:
-        if (plan->maxw > 10)
-          e = two ? launch_i8<0, 19, 2>(plan, in, batch, o, st) : launch_i8<0, 19, 1>(plan, in, batch, o, st);
-        else
-          e = two ? launch_i8<0, 10, 2>(plan, in, batch, o, st) : launch_i8<0, 10, 1>(plan, in, batch, o, st);
-    }
-  } else {
-    return fail(NRLDPC_EINVAL, "precision not implemented");
-  }
+  if (plan->precision != NRLDPC_INT8) return fail(NRLDPC_EINVAL, "precision not implemented");
+  const cudaError_t e = launch_shape(plan, plan->main, static_cast<const int8_t*>(llr), batch, o, st);
   if (e != cudaSuccess) return cuda_fail(e, "decode launch");
   return NRLDPC_OK;
 }
 
-int nrldpc_decode(const nrldpc_plan* plan, const void* llr, int64_t batch, uint32_t* bits,
+int nrldpc_decode(nrldpc_plan* plan, const void* llr, int64_t batch, uint32_t* bits,
                   int32_t* iters, int32_t* synd, uint8_t* success, uint8_t* crc_ok, int32_t* trace_w,
                   float* trace_m, int32_t* status, void* stream) {
   g_launches = 0;
@@ -1080,7 +1233,7 @@ int nrldpc_decode_host(nrldpc_plan* plan, const void* llr_host, int64_t batch, u
   NR_CUDA(cudaSetDevice(plan->device));
   const size_t esz = plan->precision == NRLDPC_INT8 ? 1 : (plan->precision == NRLDPC_F16 ? 2 : 4);
   const size_t n_c = (size_t)plan->n_blocks * plan->z;
-  const size_t words = plan->kp.words;
+  const size_t words = plan->base.words;
   const size_t per_cw_in = n_c * esz;
   const size_t per_cw_out = words * 4 + 4 + 4 + 1 + 1;
   const size_t need = align16(batch * per_cw_in) + align16(batch * words * 4) + align16(batch * 4) * 2 +
@@ -1106,7 +1259,7 @@ int nrldpc_decode_host(nrldpc_plan* plan, const void* llr_host, int64_t batch, u
   NR_CUDA(cudaMemsetAsync(d_status, 0, 4, plan->streams[0]));
   NR_CUDA(cudaStreamSynchronize(plan->streams[0]));
   if (chunks < 1) chunks = 1;
-  const int64_t per_lane_cta = (int64_t)plan->groups * plan->lanes;
+  const int64_t per_lane_cta = (int64_t)plan->main.groups * plan->main.lanes;
   int64_t chunk = (batch + chunks - 1) / chunks;
   chunk = (chunk + per_lane_cta - 1) / per_lane_cta * per_lane_cta;
   int launches = 0;

@@ -29,10 +29,11 @@
 #define NR_MAX_ROWS 46
 #define NR_MAX_EDGES 316
 #define NR_MAX_BLOCKS 68
+#define NR_MAX_TAB 456
 
 namespace nr {
 
-struct KParams {
+struct alignas(16) KParams {
   int z;
   int k_b;
   int rows;          // rows_used
@@ -44,6 +45,7 @@ struct KParams {
   int crc_len;
   uint32_t crc_poly;
   int trace;         // nonzero: record per-iteration trace, never exit early
+  int vec_load;      // rows are 16-byte aligned: vectorized prologue
   int words;         // ceil(K/32)
   long long batch;
   uint32_t l_bytes;  // per group: n_blocks*z*LANES rounded up to 16
@@ -52,9 +54,15 @@ struct KParams {
   int e_reg;         // edges whose messages live in registers (rows < nreg)
   uint32_t magic;    // 0x64646464: PRMT filler byte (half exponent of 1024)
   uint32_t one;      // 0x3C003C00: half2 {1.0, 1.0}
-  uint16_t row_start[NR_MAX_ROWS + 1];
-  uint16_t shift_l[NR_MAX_EDGES];   // shift * LANES (bytes)
-  uint32_t colbase[NR_MAX_EDGES];   // col * z * LANES (bytes)
+  uint16_t row_start[NR_MAX_ROWS + 1];  // first edge of each row (message offsets)
+  uint16_t tab_start[NR_MAX_ROWS + 1];  // row's first slot in sh/cb (multiple of 4)
+  uint8_t bar_after[NR_MAX_ROWS];       // 0: next row is column-disjoint from this layer
+  // per row: x = tab_start | w << 16, y = first smem message slot | bar_after << 16
+  alignas(8) uint2 rowdesc[NR_MAX_ROWS + 1];
+  // per-edge graph tables, each row padded to a multiple of 4 slots so a row
+  // loads them with 128-bit uniform constant loads
+  alignas(16) uint32_t sh[NR_MAX_TAB];  // shift * LANES (bytes)
+  alignas(16) uint32_t cb[NR_MAX_TAB];  // col * z * LANES (bytes)
   int beta_mode;                    // 1: half-arithmetic beta (beta_h, ndelta_h, c_h)
   uint32_t beta_h, ndelta_h, c_h;   // half2 constants of the arithmetic beta rule
   uint16_t lut[128];                // floor(beta*m) as half bits, m = 0..127
