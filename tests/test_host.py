@@ -196,3 +196,25 @@ def test_beta_half_arithmetic_rule_is_exact(beta):
     fma = u.astype(np.float64) * np.float64(np.float16(bh.value)) + c.value  # exact product+sum
     rounded = fma.astype(np.float16).astype(np.float64)                      # one rounding
     assert np.array_equal(rounded - c.value, np.floor(beta * m))
+
+
+def test_install_into_reference_package_rebinds_and_restores():
+    """The drop-in rebinds every call site of ldpclab's hot path (no GPU call)."""
+    ref = Path("/root/reference/pkg/src")
+    if not ref.is_dir():
+        pytest.skip("reference package not mounted (GPU box)")
+    import sys
+    sys.path.insert(0, str(ref))
+    try:
+        import ldpclab
+        import ldpclab.harness
+        from paper_2009_05534_b200 import integrate
+        orig = ldpclab.decoder.decode
+        patched = integrate.install_into_ldpclab()
+        assert {"ldpclab.decoder.decode", "ldpclab.harness.decode", "ldpclab.decode",
+                "ldpclab.channel.quantize", "ldpclab.harness.quantize"} <= set(patched)
+        assert ldpclab.decoder.decode is nr.decode and ldpclab.harness.decode is nr.decode
+        integrate.uninstall()
+        assert ldpclab.decoder.decode is orig
+    finally:
+        sys.path.remove(str(ref))
