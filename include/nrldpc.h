@@ -89,6 +89,15 @@ int nrldpc_quantize(const nrldpc_plan* plan, const void* llr_in, int in_dtype,
                     int out_mode, void* stream);
 
 /*
+ * Soft demapper fused into the quantizer (channel.py:57-61 then 64-83):
+ * symbols are received BPSK samples y (batch, n_tx); L = (2.0*y)/(sigma*sigma)
+ * in float64, then exactly nrldpc_quantize's mapping.
+ */
+int nrldpc_demap_quantize(const nrldpc_plan* plan, const void* symbols, int in_dtype,
+                          int64_t batch, double sigma, double scale, double clip, void* out,
+                          int out_mode, void* stream);
+
+/*
  * Layered min-sum decode (decoder.py:486-566). All pointers are device
  * pointers; asynchronous on `stream`. The plan caches per-device launch
  * data (occupancy) on first use; decode calls on one plan from several host

@@ -18,7 +18,8 @@ from .basegraph import (
     lifting_set_index,
     load_basegraph,
 )
-from .channel import QuantConfig, bpsk_awgn, bpsk_exact, demap_llr, ebn0_to_sigma, quantize
+from .channel import (QuantConfig, bpsk_awgn, bpsk_exact, demap_llr, demap_quantize, ebn0_to_sigma,
+                      quantize)
 from .codec import crc_attach, crc_check, encode_batch, syndrome_weights
 from .decoder import (
     DecodeConfig,
@@ -35,7 +36,7 @@ from .decoder import (
 __all__ = [
     "ALL_LIFTING_SIZES", "LIFTING_SETS", "BaseGraph", "CodeParams", "code_params", "edge_tables",
     "lifting_set_index", "load_basegraph", "QuantConfig", "bpsk_awgn", "bpsk_exact", "demap_llr",
-    "ebn0_to_sigma", "quantize", "crc_attach", "crc_check", "encode_batch", "syndrome_weights",
+    "ebn0_to_sigma", "quantize", "demap_quantize", "crc_attach", "crc_check", "encode_batch", "syndrome_weights",
     "DecodeConfig", "DecodeResult", "EarlyStop", "Plan", "Precision", "Strategy", "decode",
     "get_plan", "unpack_bits",
 ]

@@ -29,6 +29,7 @@ EXPORTS = (
     "nrldpc_plan_destroy",
     "nrldpc_plan_info",
     "nrldpc_quantize",
+    "nrldpc_demap_quantize",
     "nrldpc_decode",
     "nrldpc_decode_host",
     "nrldpc_launch_count",
@@ -70,6 +71,9 @@ def load() -> ctypes.CDLL:
     lib.nrldpc_quantize.argtypes = [c_void_p, c_void_p, c_int, c_int64, c_double, c_double, c_void_p,
                                     c_int, c_void_p]
     lib.nrldpc_quantize.restype = c_int
+    lib.nrldpc_demap_quantize.argtypes = [c_void_p, c_void_p, c_int, c_int64, c_double, c_double,
+                                          c_double, c_void_p, c_int, c_void_p]
+    lib.nrldpc_demap_quantize.restype = c_int
     lib.nrldpc_decode.argtypes = [c_void_p, c_void_p, c_int64] + [c_void_p] * 8 + [c_void_p]
     lib.nrldpc_decode.restype = c_int
     lib.nrldpc_decode_host.argtypes = [c_void_p, c_void_p, c_int64] + [c_void_p] * 5 + [c_int]

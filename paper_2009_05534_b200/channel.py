@@ -77,6 +77,18 @@ def _quant_plan(params):
 def quantize(llrs, cfg: QuantConfig, params):
     """Depuncture + quantize on the GPU. numpy in -> numpy out; a CUDA tensor
     in -> CUDA tensor out (asynchronous on the current stream)."""
+    return _quantize(llrs, cfg, params, None)
+
+
+def demap_quantize(symbols, sigma: float, cfg: QuantConfig, params):
+    """Fused soft demapper + quantize (channel.py:57-61 then 64-83) on the
+    GPU: received BPSK symbols in, decoder-domain LLR blocks out."""
+    if sigma <= 0:
+        raise ValueError("sigma must be positive")
+    return _quantize(symbols, cfg, params, float(sigma))
+
+
+def _quantize(llrs, cfg, params, sigma):
     import torch
     out_dtype = {"int8": torch.int8, "f16": torch.float16, "f32": torch.float32}[cfg.mode]
     is_dev = type(llrs).__module__.split(".")[0] == "torch" and llrs.is_cuda
@@ -96,8 +108,14 @@ def quantize(llrs, cfg: QuantConfig, params):
     out = torch.empty((x.shape[0], params.n_c), dtype=out_dtype, device=x.device)
     in_code = _native.IN_F64 if x.dtype == torch.float64 else _native.IN_F32
     stream = torch.cuda.current_stream(x.device).cuda_stream
-    _native.check(_native.load().nrldpc_quantize(
-        plan.handle, x.data_ptr(), in_code, int(x.shape[0]), float(cfg.scale), float(cfg.clip),
-        out.data_ptr(), _MODE[cfg.mode], ctypes.c_void_p(stream)))
+    lib = _native.load()
+    if sigma is None:
+        _native.check(lib.nrldpc_quantize(
+            plan.handle, x.data_ptr(), in_code, int(x.shape[0]), float(cfg.scale), float(cfg.clip),
+            out.data_ptr(), _MODE[cfg.mode], ctypes.c_void_p(stream)))
+    else:
+        _native.check(lib.nrldpc_demap_quantize(
+            plan.handle, x.data_ptr(), in_code, int(x.shape[0]), sigma, float(cfg.scale),
+            float(cfg.clip), out.data_ptr(), _MODE[cfg.mode], ctypes.c_void_p(stream)))
     out = out.reshape(lead + (params.n_c,))
     return out if is_dev else out.cpu().numpy()

@@ -127,67 +127,124 @@ __device__ __forceinline__ void msg_store(uint8_t* Mrow, uint32_t* mreg, int j, 
 // One layer (base row r) for thread (group, z): gather, min-sum check-node
 // update, scatter. decoder.py:295-320. t0 is the row's slot in the graph
 // tables; me0 is the row's first edge in this thread's shared-memory message
-// row.
+// row. Split in two phases so that column-disjoint rows can be interleaved
+// in one basic block (process_rows2).
+template <int MAXW, int LANES, bool REGMSG>
+struct RowWork {
+  uint32_t off[MAXW];
+  half2 t[MAXW];
+  half2 m1, m2;
+  uint32_t S;
+  uint8_t* Mrow;
+  int w;
+
+  // phase 1: gather L and the old messages, t = L - M, fold (m1, m2, S)
+  __device__ __forceinline__ void gather(const KParams& p, const int t0, const int me0, const int w_,
+                                         uint32_t zl, uint32_t ZL, const uint8_t* __restrict__ Lg,
+                                         uint8_t* __restrict__ Mz, const uint32_t* mreg, uint32_t magic) {
+    const half2 H127 = u2h(0x57F057F0u);
+    w = w_;
+    Mrow = Mz + me0 * LANES;
+    uint32_t tsh[MAXW], tcb[MAXW];
+    load_row_tables<MAXW>(p, t0, w, tsh, tcb);
+    m1 = H127;
+    m2 = H127;
+    S = 0;
+#pragma unroll
+    for (int j = 0; j < MAXW; ++j) {
+      if (j < w) {
+        off[j] = edge_offset(tsh[j], tcb[j], zl, ZL);
+        const half2 lh = unpack_elem<LANES>(ld_elem<LANES>(Lg + off[j]), magic);
+        const half2 mh = msg_load<LANES, REGMSG>(Mrow, mreg, j, j, magic);
+        const half2 tj = __hsub2(lh, mh);           // exact: L - M
+        const half2 aj = __habs2(tj);
+        m2 = __hmin2(m2, __hmax2(m1, aj));          // kernels.py:247-250
+        m1 = __hmin2(m1, aj);
+        S ^= h2u(tj);                               // sign product (bits 15/31)
+        t[j] = tj;
+      }
+    }
+  }
+
+  // beta-scaled magnitudes with the row sign folded in: b' = (-1)^S * b.
+  // Split from the scatter so that fused rows share one branch on beta_mode
+  // and their scatters stay in one basic block.
+  half2 dd, b2s;  // (b1 - b2)' and b2'
+  __device__ __forceinline__ void beta_arith(const KParams& p, uint32_t one) {
+    // floor(beta*m) == RN(beta_h*(m - delta) + C) - C for every m in [0,127]
+    // (verified exhaustively on the host); all FMA-pipe, no table lookups
+    const half2 sig = u2h((S & 0x80008000u) | one);
+    const half2 bh = u2h(p.beta_h), nd = u2h(p.ndelta_h), cc = u2h(p.c_h);
+    const half2 B1 = __hfma2(__hadd2(m1, nd), bh, cc);
+    const half2 B2 = __hfma2(__hadd2(m2, nd), bh, cc);
+    dd = __hmul2(__hsub2(B1, B2), sig);
+    b2s = __hmul2(__hsub2(B2, cc), sig);
+  }
+  __device__ __forceinline__ void beta_lut(const uint16_t* __restrict__ lut, uint32_t one) {
+    const half2 sig = u2h((S & 0x80008000u) | one);
+    const half2 b1 = beta_lut2(lut, m1);
+    const half2 b2 = beta_lut2(lut, m2);
+    dd = __hmul2(__hsub2(b1, b2), sig);
+    b2s = __hmul2(b2, sig);
+  }
+
+  // phase 2: new messages and posteriors, scatter
+  __device__ __forceinline__ void scatter(uint8_t* __restrict__ Lg, uint32_t* mreg, uint32_t one,
+                                          bool st_ok) {
+    const half2 H127 = u2h(0x57F057F0u);   // 127.0
+    const half2 H1152 = u2h(0x64806480u);  // 1152.0
+#pragma unroll
+    for (int j = 0; j < MAXW; ++j) {
+      if (j < w) {
+        // x = 0 for the edge holding the minimum (it gets m2; a tie implies
+        // m1 == m2), else 1: |t| - m1 is a non-negative integer, saturated.
+        const half2 x = __hsub2_sat(__habs2(t[j]), m1);
+        const half2 mag = __hfma2(x, dd, b2s);       // +-b1 or +-b2
+        // L' = sign(t) * min(|clamp t| + mag', 127) == clamp127(t + out), using
+        // min(|t|,127) + mag' = min(|t| + mag', 127 + mag')
+        const half2 y = __hmin2(__hmin2(__hadd2(__habs2(t[j]), mag), __hadd2(mag, H127)), H127);
+        const half2 sg = u2h((h2u(t[j]) & 0x80008000u) | one);
+        st_elem_if<LANES>(Lg + off[j], pack_elem<LANES>(__hfma2(y, sg, H1152)), st_ok);
+        msg_store<LANES, REGMSG>(Mrow, mreg, j, j, __hfma2(mag, sg, H1152), st_ok);
+      }
+    }
+  }
+};
+
 template <int MAXW, int LANES, bool REGMSG>
 __device__ __forceinline__ void process_row(const KParams& p, const int t0, const int me0, const int w,
                                             uint32_t zl, uint32_t ZL, uint8_t* __restrict__ Lg,
                                             uint8_t* __restrict__ Mz, uint32_t* mreg,
                                             const uint16_t* __restrict__ lut, uint32_t magic,
                                             uint32_t one, bool st_ok) {
-  const half2 H127 = u2h(0x57F057F0u);   // 127.0
-  const half2 H1152 = u2h(0x64806480u);  // 1152.0
-  uint8_t* Mrow = Mz + me0 * LANES;
-  uint32_t off[MAXW], tsh[MAXW], tcb[MAXW];
-  load_row_tables<MAXW>(p, t0, w, tsh, tcb);
-  half2 t[MAXW];
-  half2 m1 = H127, m2 = H127;
-  uint32_t S = 0;
-#pragma unroll
-  for (int j = 0; j < MAXW; ++j) {
-    if (j < w) {
-      off[j] = edge_offset(tsh[j], tcb[j], zl, ZL);
-      const half2 lh = unpack_elem<LANES>(ld_elem<LANES>(Lg + off[j]), magic);
-      const half2 mh = msg_load<LANES, REGMSG>(Mrow, mreg, j, j, magic);
-      const half2 tj = __hsub2(lh, mh);           // exact: L - M
-      const half2 aj = __habs2(tj);
-      m2 = __hmin2(m2, __hmax2(m1, aj));          // kernels.py:247-250
-      m1 = __hmin2(m1, aj);
-      S ^= h2u(tj);                               // sign product (bits 15/31)
-      t[j] = tj;
-    }
-  }
-  // beta-scaled magnitudes with the row sign folded in: b' = (-1)^S * b
-  const half2 sig = u2h((S & 0x80008000u) | one);
-  half2 dd, b2s;  // (b1 - b2)' and b2'
+  RowWork<MAXW, LANES, REGMSG> r;
+  r.gather(p, t0, me0, w, zl, ZL, Lg, Mz, mreg, magic);
+  if (p.beta_mode) r.beta_arith(p, one);
+  else r.beta_lut(lut, one);
+  r.scatter(Lg, mreg, one, st_ok);
+}
+
+// Two consecutive column-disjoint rows as one basic block: no barrier between
+// them is needed and the scheduler interleaves their independent chains.
+template <int WA, int WB, int LANES>
+__device__ __forceinline__ void process_rows2(const KParams& p, int t0a, int me0a, int t0b, int me0b,
+                                              uint32_t zl, uint32_t ZL, uint8_t* __restrict__ Lg,
+                                              uint8_t* __restrict__ Mz, uint32_t* mreg,
+                                              const uint16_t* __restrict__ lut, uint32_t magic,
+                                              uint32_t one, bool st_ok) {
+  RowWork<WA, LANES, false> a;
+  RowWork<WB, LANES, false> b;
+  a.gather(p, t0a, me0a, WA, zl, ZL, Lg, Mz, mreg, magic);
+  b.gather(p, t0b, me0b, WB, zl, ZL, Lg, Mz, mreg, magic);
   if (p.beta_mode) {
-    // floor(beta*m) == RN(beta_h*(m - delta) + C) - C for every m in [0,127]
-    // (verified exhaustively on the host); all FMA-pipe, no table lookups
-    const half2 bh = u2h(p.beta_h), nd = u2h(p.ndelta_h), cc = u2h(p.c_h);
-    const half2 B1 = __hfma2(__hadd2(m1, nd), bh, cc);
-    const half2 B2 = __hfma2(__hadd2(m2, nd), bh, cc);
-    dd = __hmul2(__hsub2(B1, B2), sig);
-    b2s = __hmul2(__hsub2(B2, cc), sig);
+    a.beta_arith(p, one);
+    b.beta_arith(p, one);
   } else {
-    const half2 b1 = beta_lut2(lut, m1);
-    const half2 b2 = beta_lut2(lut, m2);
-    dd = __hmul2(__hsub2(b1, b2), sig);
-    b2s = __hmul2(b2, sig);
+    a.beta_lut(lut, one);
+    b.beta_lut(lut, one);
   }
-#pragma unroll
-  for (int j = 0; j < MAXW; ++j) {
-    if (j < w) {
-      // x = 0 for the edge holding the minimum (it gets m2; a tie implies
-      // m1 == m2), else 1: |t| - m1 is a non-negative integer, saturated.
-      const half2 x = __hsub2_sat(__habs2(t[j]), m1);
-      const half2 mag = __hfma2(x, dd, b2s);       // +-b1 or +-b2
-      // L' = sign(t) * min(|clamp t| + mag', 127) == clamp127(t + out), using
-      // min(|t|,127) + mag' = min(|t| + mag', 127 + mag')
-      const half2 y = __hmin2(__hmin2(__hadd2(__habs2(t[j]), mag), __hadd2(mag, H127)), H127);
-      const half2 sg = u2h((h2u(t[j]) & 0x80008000u) | one);
-      st_elem_if<LANES>(Lg + off[j], pack_elem<LANES>(__hfma2(y, sg, H1152)), st_ok);
-      msg_store<LANES, REGMSG>(Mrow, mreg, j, j, __hfma2(mag, sg, H1152), st_ok);
-    }
-  }
+  a.scatter(Lg, mreg, one, st_ok);
+  b.scatter(Lg, mreg, one, st_ok);
 }
 
 // Syndrome weight (decoder.py:323-329) and min|L| (decoder.py:480-483) over
@@ -278,6 +335,29 @@ __device__ __forceinline__ void dispatch_w(int w, F&& f) {
     else if (weq(w, 8)) f(IC<8>{});
     else if (weq(w, 10)) f(IC<10>{});
   }
+}
+
+// Fused pairs of column-disjoint rows that occur in the base graphs
+// (BG1 rows 16..45, BG2 rows 11..41); returns false if (wa, wb) has no
+// compiled body (the caller then runs the two rows back to back).
+template <int BG, typename F>
+__device__ __forceinline__ bool dispatch_pair(int wa, int wb, F&& f) {
+  if constexpr (BG == 1) {
+    if (weq(wa, 5) && weq(wb, 5)) f(IC<5>{}, IC<5>{});
+    else if (weq(wa, 6) && weq(wb, 6)) f(IC<6>{}, IC<6>{});
+    else if (weq(wa, 5) && weq(wb, 4)) f(IC<5>{}, IC<4>{});
+    else if (weq(wa, 4) && weq(wb, 5)) f(IC<4>{}, IC<5>{});
+    else if (weq(wa, 6) && weq(wb, 5)) f(IC<6>{}, IC<5>{});
+    else return false;
+  } else {
+    if (weq(wa, 4) && weq(wb, 4)) f(IC<4>{}, IC<4>{});
+    else if (weq(wa, 4) && weq(wb, 3)) f(IC<4>{}, IC<3>{});
+    else if (weq(wa, 5) && weq(wb, 3)) f(IC<5>{}, IC<3>{});
+    else if (weq(wa, 5) && weq(wb, 4)) f(IC<5>{}, IC<4>{});
+    else if (weq(wa, 3) && weq(wb, 4)) f(IC<3>{}, IC<4>{});
+    else return false;
+  }
+  return true;
 }
 
 // Register-resident messages (BG1 pairs at the largest Z, see choose_shape):
@@ -372,6 +452,23 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
       const int t0 = (int)(d.x & 0xFFFFu);
       const int w = (int)(d.x >> 16);
       const int me0 = (int)(d.y & 0xFFFFu);
+      if ((d.y >> 16) == 0 && r + 1 < p.rows) {
+        // rows r and r+1 share no column: one fused body when compiled
+        const int t0b = (int)(nd.x & 0xFFFFu);
+        const int wb = (int)(nd.x >> 16);
+        const int me0b = (int)(nd.y & 0xFFFFu);
+        const bool fused = dispatch_pair<BG>(w, wb, [&](auto WA, auto WB) {
+          process_rows2<decltype(WA)::value, decltype(WB)::value, LANES>(
+              p, t0, me0, t0b, me0b, c.zl, c.ZL, c.Lg, c.Mz, rm.r4, c.lut, c.magic, c.one, c.st_ok);
+        });
+        if (fused) {
+          ++r;
+          const uint2 d2 = nd;
+          nd = p.rowdesc[r + 1];
+          if (d2.y >> 16) __syncthreads();
+          continue;
+        }
+      }
       dispatch_w<BG>(w, [&](auto W) {
         process_row<decltype(W)::value, LANES, false>(p, t0, me0, decltype(W)::value, c.zl, c.ZL, c.Lg,
                                                       c.Mz, rm.r4, c.lut, c.magic, c.one, c.st_ok);
@@ -432,21 +529,21 @@ __device__ __forceinline__ void write_bits(const KParams& p, const uint8_t* __re
   }
 }
 
-// Bit-serial CRC over the K hard bits (codec.py:183-213); true when the
-// register drains to zero.
+// CRC over the K hard bits (codec.py:183-213) computed by the whole group.
+// The bit-serial register is linear over GF(2): after all K bits it equals
+// XOR over set bits i of rem(x^(K-1-i+L), g), tabulated on the host
+// (crc_tab[i]). Each thread folds positions i = z, z+Z, ... and XORs its
+// partial into the group's accumulator; the check passes when the XOR is 0.
 template <int LANES>
-__device__ bool crc_ok_serial(const KParams& p, const uint8_t* __restrict__ Lg, int lane) {
+__device__ __forceinline__ uint32_t crc_partial(const KParams& p, const uint8_t* __restrict__ Lg, int z,
+                                                int lane) {
   const int K = p.k_b * p.z;
-  if (K < p.crc_len) return false;
-  const uint32_t top = 1u << (p.crc_len - 1);
-  const uint32_t mask = (p.crc_len == 32) ? 0xFFFFFFFFu : ((1u << p.crc_len) - 1u);
-  uint32_t reg = 0;
-  for (int i = 0; i < K; ++i) {
-    const uint32_t bit = Lg[i * LANES + lane] < 128u ? 1u : 0u;
-    const uint32_t fb = ((reg & top) ? 1u : 0u) ^ bit;
-    reg = ((reg << 1) & mask) ^ (fb ? p.crc_poly : 0u);
+  uint32_t acc = 0;
+  for (int i = z; i < K; i += p.z) {
+    const uint32_t neg = Lg[i * LANES + lane] < 128u ? 0xFFFFFFFFu : 0u;
+    acc ^= __ldg(p.crc_tab + i) & neg;
   }
-  return reg == 0;
+  return acc;
 }
 
 // Layered decode of G groups x LANES codewords per CTA, everything resident
@@ -585,13 +682,18 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
         cand[l] = lane_valid[l] && !gs.done[l] && gs.synd[l] == 0 && gs.minabs[l] > 0;
     }
     if (p.early_stop == NRLDPC_STOP_CRC) {
-      if (active && z == 0) {
+      if (active) {
 #pragma unroll
-        for (int l = 0; l < LANES; ++l) gs.accept[l] = cand[l] ? (int)crc_ok_serial<LANES>(p, Lg, l) : 0;
+        for (int l = 0; l < LANES; ++l) {
+          if (cand[l]) {
+            const uint32_t part = p.crc_tab ? crc_partial<LANES>(p, Lg, z, l) : 1u;
+            if (part) atomicXor(reinterpret_cast<unsigned int*>(&gs.accept[l]), part);
+          }
+        }
       }
       __syncthreads();
 #pragma unroll
-      for (int l = 0; l < LANES; ++l) cand[l] = cand[l] && gs.accept[l];
+      for (int l = 0; l < LANES; ++l) cand[l] = cand[l] && p.crc_tab != nullptr && gs.accept[l] == 0;
     }
     int fin[2] = {0, 0};  // not frozen at the last iteration: final values
     if (active && last) {
@@ -639,6 +741,7 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
         }
         gs.synd[l] = 0;
         gs.minabs[l] = 255;
+        gs.accept[l] = 0;
       }
       if (newly) atomicAdd(&cta->n_done, newly);
     }
@@ -651,10 +754,13 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
 
 // ---- quantize: depuncture + channel-domain -> decoder-domain LLRs ---------
 // channel.py:64-83; arithmetic in float64 like the reference.
-template <typename Tin, int MODE>
+// With DEMAP the input is received BPSK symbols y and the LLR is formed first
+// exactly as channel.demap_llr does it: (2.0 * y) / (sigma * sigma), float64
+// (channel.py:57-61), with sigma2 = sigma*sigma computed on the host.
+template <typename Tin, int MODE, bool DEMAP = false>
 __global__ void __launch_bounds__(256) k_quantize(const Tin* __restrict__ in, long long batch, int n_tx,
                                                   int n_c, int two_z, double scale, double clip,
-                                                  void* __restrict__ out) {
+                                                  void* __restrict__ out, double sigma2 = 1.0) {
   const long long total = batch * (long long)n_c;
   const long long stride = (long long)gridDim.x * blockDim.x * 4;
   for (long long i0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4; i0 < total; i0 += stride) {
@@ -664,7 +770,8 @@ __global__ void __launch_bounds__(256) k_quantize(const Tin* __restrict__ in, lo
       if (i >= total) break;
       const long long b = i / n_c;
       const int j = (int)(i - b * n_c);
-      const double v = j < two_z ? 0.0 : (double)in[b * n_tx + (j - two_z)];
+      double v = j < two_z ? 0.0 : (double)in[b * n_tx + (j - two_z)];
+      if (DEMAP && j >= two_z) v = __ddiv_rn(__dmul_rn(2.0, v), sigma2);
       if (MODE == NRLDPC_INT8) {
         double s = rint(v * scale);
         s = fmin(fmax(s, -127.0), 127.0);
@@ -727,6 +834,7 @@ struct nrldpc_plan {
   int precision = NRLDPC_INT8;
   int early_stop = NRLDPC_STOP_SYNDROME;
   int crc_kind = NRLDPC_CRC24B;
+  uint32_t* d_crc_tab = nullptr;  // device: rem(x^(K-1-i+L), g) for i < K (crc mode)
   double beta = 0.75;
   int max_iter = 20;
   int k_b = 0, z = 0, rows = 0, n_blocks = 0, n_edges = 0, maxw = 0;
@@ -1109,6 +1217,31 @@ int nrldpc_plan_create(int device, int k_b, int z, int rows_used, const int32_t*
       same = row_start[r] == (bg == 1 ? RowW<1>::e0[r] : RowW<2>::e0[r]);
     if (same) p->schedule = bg;
   }
+  if (early_stop == NRLDPC_STOP_CRC && k_b * z >= crc_len) {
+    // rem(x^(K-1-i+L), g) for i = K-1 down to 0: start at x^L mod g = poly
+    const int K = k_b * z;
+    std::vector<uint32_t> tab(K);
+    const uint32_t mask = (crc_len == 32) ? 0xFFFFFFFFu : ((1u << crc_len) - 1u);
+    uint32_t r = crc_poly & mask;
+    for (int i = K - 1; i >= 0; --i) {
+      tab[i] = r;
+      const bool top = (r >> (crc_len - 1)) & 1u;
+      r = ((r << 1) & mask) ^ (top ? crc_poly : 0u);
+    }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    ce = cudaMalloc(&p->d_crc_tab, sizeof(uint32_t) * K);
+    if (ce == cudaSuccess)
+      ce = cudaMemcpy(p->d_crc_tab, tab.data(), sizeof(uint32_t) * K, cudaMemcpyHostToDevice);
+    cudaSetDevice(prev);
+    if (ce != cudaSuccess) {
+      if (p->d_crc_tab) cudaFree(p->d_crc_tab);
+      delete p;
+      return cuda_fail(ce, "crc table");
+    }
+    p->base.crc_tab = p->d_crc_tab;
+  }
   const char* force = std::getenv("NRLDPC_FORCE_LANES");
   p->main = choose_shape(p, force && force[0] == '1' ? 1 : 2);
   // set kernel attributes and cache occupancy now, so decode never mutates
@@ -1137,6 +1270,7 @@ int nrldpc_plan_destroy(nrldpc_plan* plan) {
   for (auto& s : plan->streams)
     if (s) cudaStreamDestroy(s);
   if (plan->d_buf) cudaFree(plan->d_buf);
+  if (plan->d_crc_tab) cudaFree(plan->d_crc_tab);
   cudaSetDevice(prev);
   delete plan;
   return NRLDPC_OK;
@@ -1157,12 +1291,14 @@ int nrldpc_plan_info(const nrldpc_plan* plan, int64_t* k, int64_t* n_c, int64_t*
   return NRLDPC_OK;
 }
 
-int nrldpc_quantize(const nrldpc_plan* plan, const void* llr_in, int in_dtype, int64_t batch,
-                    double scale, double clip, void* out, int out_mode, void* stream) {
+static int quantize_impl(const nrldpc_plan* plan, const void* llr_in, int in_dtype, int64_t batch,
+                         double scale, double clip, void* out, int out_mode, void* stream, bool demap,
+                         double sigma) {
   g_launches = 0;
   if (!plan) return fail(NRLDPC_EINVAL, "plan is NULL");
   if (batch < 0) return fail(NRLDPC_EINVAL, "batch must be non-negative");
   if (!(scale > 0.0)) return fail(NRLDPC_EINVAL, "scale must be positive");
+  if (demap && !(sigma > 0.0)) return fail(NRLDPC_EINVAL, "sigma must be positive");
   if (batch == 0) return NRLDPC_OK;
   if (!llr_in || !out) return fail(NRLDPC_EINVAL, "NULL buffer");
   const int n_c = plan->n_blocks * plan->z;
@@ -1172,20 +1308,22 @@ int nrldpc_quantize(const nrldpc_plan* plan, const void* llr_in, int in_dtype, i
   const long long total = batch * (long long)n_c;
   const long long want = (total + 4 * 256 - 1) / (4 * 256);
   const int grid = (int)std::min<long long>(want, 148LL * 16);
-  auto go = [&](auto kern, auto* typed_in) {
-    kern<<<grid, 256, 0, st>>>(typed_in, (long long)batch, n_tx, n_c, 2 * plan->z, scale, clip, out);
+  const double sigma2 = sigma * sigma;
+  auto go = [&](auto k_plain, auto k_demap, auto* typed_in) {
+    if (demap) k_demap<<<grid, 256, 0, st>>>(typed_in, (long long)batch, n_tx, n_c, 2 * plan->z, scale, clip, out, sigma2);
+    else k_plain<<<grid, 256, 0, st>>>(typed_in, (long long)batch, n_tx, n_c, 2 * plan->z, scale, clip, out, 1.0);
   };
   if (in_dtype == NRLDPC_IN_F64) {
     const double* in = static_cast<const double*>(llr_in);
-    if (out_mode == NRLDPC_INT8) go(k_quantize<double, NRLDPC_INT8>, in);
-    else if (out_mode == NRLDPC_F16) go(k_quantize<double, NRLDPC_F16>, in);
-    else if (out_mode == NRLDPC_F32) go(k_quantize<double, NRLDPC_F32>, in);
+    if (out_mode == NRLDPC_INT8) go(k_quantize<double, NRLDPC_INT8, false>, k_quantize<double, NRLDPC_INT8, true>, in);
+    else if (out_mode == NRLDPC_F16) go(k_quantize<double, NRLDPC_F16, false>, k_quantize<double, NRLDPC_F16, true>, in);
+    else if (out_mode == NRLDPC_F32) go(k_quantize<double, NRLDPC_F32, false>, k_quantize<double, NRLDPC_F32, true>, in);
     else return fail(NRLDPC_EINVAL, "unknown quantize out_mode");
   } else if (in_dtype == NRLDPC_IN_F32) {
     const float* in = static_cast<const float*>(llr_in);
-    if (out_mode == NRLDPC_INT8) go(k_quantize<float, NRLDPC_INT8>, in);
-    else if (out_mode == NRLDPC_F16) go(k_quantize<float, NRLDPC_F16>, in);
-    else if (out_mode == NRLDPC_F32) go(k_quantize<float, NRLDPC_F32>, in);
+    if (out_mode == NRLDPC_INT8) go(k_quantize<float, NRLDPC_INT8, false>, k_quantize<float, NRLDPC_INT8, true>, in);
+    else if (out_mode == NRLDPC_F16) go(k_quantize<float, NRLDPC_F16, false>, k_quantize<float, NRLDPC_F16, true>, in);
+    else if (out_mode == NRLDPC_F32) go(k_quantize<float, NRLDPC_F32, false>, k_quantize<float, NRLDPC_F32, true>, in);
     else return fail(NRLDPC_EINVAL, "unknown quantize out_mode");
   } else {
     return fail(NRLDPC_EINVAL, "unknown quantize input dtype");
@@ -1193,6 +1331,17 @@ int nrldpc_quantize(const nrldpc_plan* plan, const void* llr_in, int in_dtype, i
   ++g_launches;
   NR_CUDA(cudaGetLastError());
   return NRLDPC_OK;
+}
+
+int nrldpc_quantize(const nrldpc_plan* plan, const void* llr_in, int in_dtype, int64_t batch,
+                    double scale, double clip, void* out, int out_mode, void* stream) {
+  return quantize_impl(plan, llr_in, in_dtype, batch, scale, clip, out, out_mode, stream, false, 1.0);
+}
+
+int nrldpc_demap_quantize(const nrldpc_plan* plan, const void* symbols, int in_dtype, int64_t batch,
+                          double sigma, double scale, double clip, void* out, int out_mode,
+                          void* stream) {
+  return quantize_impl(plan, symbols, in_dtype, batch, scale, clip, out, out_mode, stream, true, sigma);
 }
 
 static int decode_impl(nrldpc_plan* plan, const void* llr, int64_t batch, const KOut& o,

@@ -58,11 +58,12 @@ struct alignas(16) KParams {
   uint16_t tab_start[NR_MAX_ROWS + 1];  // row's first slot in sh/cb (multiple of 4)
   uint8_t bar_after[NR_MAX_ROWS];       // 0: next row is column-disjoint from this layer
   // per row: x = tab_start | w << 16, y = first smem message slot | bar_after << 16
-  alignas(8) uint2 rowdesc[NR_MAX_ROWS + 1];
+  alignas(8) uint2 rowdesc[NR_MAX_ROWS + 2];
   // per-edge graph tables, each row padded to a multiple of 4 slots so a row
   // loads them with 128-bit uniform constant loads
   alignas(16) uint32_t sh[NR_MAX_TAB];  // shift * LANES (bytes)
   alignas(16) uint32_t cb[NR_MAX_TAB];  // col * z * LANES (bytes)
+  const uint32_t* crc_tab;          // crc mode: rem(x^(K-1-i+L), g), device memory
   int beta_mode;                    // 1: half-arithmetic beta (beta_h, ndelta_h, c_h)
   uint32_t beta_h, ndelta_h, c_h;   // half2 constants of the arithmetic beta rule
   uint16_t lut[128];                // floor(beta*m) as half bits, m = 0..127

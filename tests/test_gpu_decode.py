@@ -195,3 +195,33 @@ def test_native_library_is_the_compute_path(cuda_ok):
     bg = nr.load_basegraph("BG2", 64)
     nr.decode(np.zeros((4, 3328), np.int8), bg, nr.DecodeConfig(max_iter=2))
     assert _native.launch_count() >= 1
+
+
+def test_demap_quantize_matches_reference_chain(cuda_ok):
+    """Fused demapper+quantizer == channel.demap_llr then channel.quantize."""
+    for bg_id, z, rows in (("BG1", 384, 46), ("BG2", 13, 42)):
+        bg = nr.load_basegraph(bg_id, z)
+        params = nr.code_params(bg, z, rows)
+        rng = np.random.default_rng(z)
+        sigma = nr.ebn0_to_sigma(1.0, params.k / params.n_tx)
+        y = nr.bpsk_awgn(rng.integers(0, 2, size=(5, params.n_tx)), sigma, rng)
+        ref = oracle.quantize_i8(nr.demap_llr(y, sigma), z)          # channel.py:57-61, 64-83
+        got = nr.demap_quantize(y, sigma, nr.QuantConfig(), params)
+        assert np.array_equal(got, ref)
+        dev = nr.demap_quantize(torch.from_numpy(y).cuda(), sigma, nr.QuantConfig(), params)
+        assert np.array_equal(dev.cpu().numpy(), ref)
+
+
+def test_crc_at_full_size_vs_oracle(cuda_ok):
+    """Group-parallel CRC-24B over K=8448 hard bits (crc table path)."""
+    bg = nr.load_basegraph("BG1", 384)
+    params = nr.code_params(bg, 384, 46)
+    rng = np.random.default_rng(21)
+    msgs = np.stack([nr.crc_attach(rng.integers(0, 2, params.k - 24, dtype=np.uint8), k=params.k)
+                     for _ in range(24)])
+    msgs[5, 100] ^= 1  # one codeword whose payload no longer matches its CRC
+    tx = nr.encode_batch(msgs, bg, 384, 46)[:, 768:]
+    sigma = nr.ebn0_to_sigma(2.5, params.k / params.n_tx)
+    blocks = oracle.quantize_i8(nr.demap_llr(nr.bpsk_awgn(tx, sigma, rng), sigma), 384)
+    res = _oracle_cmp(bg, 46, nr.DecodeConfig(max_iter=12, early_stop="crc"), blocks)
+    assert not res.crc_ok[5] and res.crc_ok.sum() >= 4  # int8 at scale 8 converges for some
