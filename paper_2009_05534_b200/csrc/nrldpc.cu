@@ -815,6 +815,8 @@ __global__ void __launch_bounds__(512) k_alu_peak(uint32_t* out, int iters, uint
 
 }  // namespace nr
 
+#include "nrldpc_float.cuh"
+
 // ---------------------------------------------------------------------------
 // Host side
 
@@ -963,6 +965,40 @@ void find_beta_arith(double beta, KParams* kp) {
 // fits on chip; for BG1 at the largest Z the first rows' messages move from
 // shared memory into registers to make room. Smaller CTAs keep the per-layer
 // barrier cheap; more codewords per SM come from more CTAs.
+// Float engines: 4 bytes per position per group (one f32 codeword, or a
+// half2 pair of f16 codewords); messages go to a global workspace.
+Shape choose_shape_float(const nrldpc_plan* p) {
+  const size_t smem_max = 232448;
+  const size_t lb = align16((size_t)p->n_blocks * p->z * 4);
+  auto smem_f = [&](int g) { return (size_t)16 + 16 + sizeof(FltState) * g + g * lb; };
+  int best_g = 1;
+  double best_waste = 1e9;
+  for (int g = 1; g * p->z <= 512; ++g) {
+    if (smem_f(g) > smem_max) break;
+    const int thr = g * p->z, thr32 = (thr + 31) / 32 * 32;
+    const double waste = double(thr32 - thr) / thr32;
+    if (thr32 < 64 && (g + 1) * p->z <= 512 && smem_f(g + 1) <= smem_max) continue;
+    if (waste < best_waste - 1e-9) {
+      best_waste = waste;
+      best_g = g;
+    }
+    if (waste <= 1.0 / 16) break;
+  }
+  Shape sh;
+  sh.lanes = p->precision == NRLDPC_F16 ? 2 : 1;
+  sh.groups = best_g;
+  sh.threads = (best_g * p->z + 31) / 32 * 32;
+  sh.smem = smem_f(best_g);
+  sh.kp = p->base;
+  sh.kp.groups = best_g;
+  sh.kp.l_bytes = (uint32_t)lb;
+  for (int t = 0; t < NR_MAX_TAB; ++t) {
+    sh.kp.sh[t] = p->base.sh[t] * 4u;
+    sh.kp.cb[t] = p->base.cb[t] * (uint32_t)p->z * 4u;
+  }
+  return sh;
+}
+
 Shape choose_shape(const nrldpc_plan* p, int max_lanes) {
   const size_t smem_max = 232448;
   const size_t n_pos = (size_t)p->n_blocks * p->z;
@@ -1052,6 +1088,40 @@ static cudaError_t launch_shape(const nrldpc_plan* plan, Shape& sh, const int8_t
   }
 }
 
+template <int PREC>
+static cudaError_t launch_float(Shape& sh, int device, const void* llr, long long batch, const KOut& o,
+                                cudaStream_t st) {
+  static bool attr_done[64] = {};
+  auto kern = k_decode_flt<PREC>;
+  if (!attr_done[device & 63]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    if (e != cudaSuccess) return e;
+    attr_done[device & 63] = true;
+  }
+  if (!sh.occ) {
+    int occ = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, sh.threads, sh.smem);
+    if (e != cudaSuccess) return e;
+    sh.occ = occ > 0 ? occ : 1;
+  }
+  if (!llr) return cudaSuccess;
+  KParams kp = sh.kp;
+  kp.batch = batch;
+  kp.trace = o.trace_w != nullptr;
+  const long long per_cta = (long long)sh.groups * sh.lanes;
+  const long long grid = (batch + per_cta - 1) / per_cta;
+  // messages: stream-ordered workspace, [group][edge][z] x 4 bytes
+  uint32_t* ws = nullptr;
+  const size_t ws_bytes = (size_t)grid * sh.groups * kp.n_edges * kp.z * 4;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws), ws_bytes, st);
+  if (e != cudaSuccess) return e;
+  kern<<<(unsigned)grid, sh.threads, sh.smem, st>>>(kp, llr, ws, o);
+  ++g_launches;
+  e = cudaGetLastError();
+  const cudaError_t f = cudaFreeAsync(ws, st);
+  return e != cudaSuccess ? e : f;
+}
+
 extern "C" {
 
 const char* nrldpc_last_error(void) { return g_last_error.c_str(); }
@@ -1124,8 +1194,8 @@ int nrldpc_plan_create(int device, int k_b, int z, int rows_used, const int32_t*
     return fail(NRLDPC_EINVAL, "rows_used must be in [4, 46]");
   if (!(beta > 0.0 && beta <= 1.0)) return fail(NRLDPC_EINVAL, "beta must be in (0, 1]");
   if (max_iter < 1) return fail(NRLDPC_EINVAL, "max_iter must be at least 1");
-  if (precision != NRLDPC_INT8)
-    return fail(NRLDPC_EINVAL, "only int8 precision is implemented on the device path");
+  if (precision != NRLDPC_INT8 && precision != NRLDPC_F16 && precision != NRLDPC_F32)
+    return fail(NRLDPC_EINVAL, "unknown precision");
   if (early_stop < NRLDPC_STOP_SYNDROME || early_stop > NRLDPC_STOP_NONE)
     return fail(NRLDPC_EINVAL, "unknown early_stop mode");
   int crc_len = 0;
@@ -1243,7 +1313,20 @@ int nrldpc_plan_create(int device, int k_b, int z, int rows_used, const int32_t*
     p->base.crc_tab = p->d_crc_tab;
   }
   const char* force = std::getenv("NRLDPC_FORCE_LANES");
-  p->main = choose_shape(p, force && force[0] == '1' ? 1 : 2);
+  if (precision == NRLDPC_INT8) {
+    p->main = choose_shape(p, force && force[0] == '1' ? 1 : 2);
+  } else {
+    p->main = choose_shape_float(p);
+    if (precision == NRLDPC_F32) {
+      const float bf = (float)beta;  // np.float32(beta)
+      std::memcpy(&p->main.kp.beta_f, &bf, 4);
+    } else {
+      const __half bh = __double2half(beta);  // np.float16(beta): one RNE rounding
+      uint16_t u;
+      std::memcpy(&u, &bh, 2);
+      p->main.kp.beta_f = (uint32_t)u * 0x10001u;
+    }
+  }
   // set kernel attributes and cache occupancy now, so decode never mutates
   // the plan (concurrent decodes on one plan are then race-free)
   {
@@ -1251,7 +1334,10 @@ int nrldpc_plan_create(int device, int k_b, int z, int rows_used, const int32_t*
     cudaGetDevice(&prev);
     cudaSetDevice(device);
     KOut none{};
-    const cudaError_t e1 = launch_shape(p, p->main, nullptr, 0, none, nullptr);
+    const cudaError_t e1 =
+        precision == NRLDPC_INT8 ? launch_shape(p, p->main, nullptr, 0, none, nullptr)
+        : precision == NRLDPC_F32 ? launch_float<NRLDPC_F32>(p->main, device, nullptr, 0, none, nullptr)
+                                  : launch_float<NRLDPC_F16>(p->main, device, nullptr, 0, none, nullptr);
     cudaSetDevice(prev);
     if (e1 != cudaSuccess) {
       delete p;
@@ -1346,7 +1432,13 @@ int nrldpc_demap_quantize(const nrldpc_plan* plan, const void* symbols, int in_d
 
 static int decode_impl(nrldpc_plan* plan, const void* llr, int64_t batch, const KOut& o,
                        cudaStream_t st) {
-  if (plan->precision != NRLDPC_INT8) return fail(NRLDPC_EINVAL, "precision not implemented");
+  if (plan->precision != NRLDPC_INT8) {
+    const cudaError_t e = plan->precision == NRLDPC_F32
+                              ? launch_float<NRLDPC_F32>(plan->main, plan->device, llr, batch, o, st)
+                              : launch_float<NRLDPC_F16>(plan->main, plan->device, llr, batch, o, st);
+    if (e != cudaSuccess) return cuda_fail(e, "decode launch");
+    return NRLDPC_OK;
+  }
   const cudaError_t e = launch_shape(plan, plan->main, static_cast<const int8_t*>(llr), batch, o, st);
   if (e != cudaSuccess) return cuda_fail(e, "decode launch");
   return NRLDPC_OK;

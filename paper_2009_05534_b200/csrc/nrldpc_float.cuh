@@ -1,0 +1,304 @@
+// Floating-point layered min-sum engines (Precision.F32 / Precision.F16),
+// bit-exact restatements of the reference's float paths:
+//   f32: lvc = lv - msg, b = float32(beta) * m, new = lvc + out, no clamp
+//   f16: every op rounded to half (numpy float16 ufuncs are correctly
+//        rounded), lvc and new clamped to +-65504 (decoder.py:227-240)
+// (/root/reference/pkg/src/ldpclab/decoder.py:295-320). f16 carries two
+// codewords per half2 lane; f32 one codeword per thread. Posteriors live in
+// shared memory (4 bytes per position per group); messages (4 bytes per edge
+// and z per group) live in a stream-ordered global workspace, coalesced as
+// [group][edge][z]. Included by nrldpc.cu.
+#pragma once
+
+namespace nr {
+
+// Per-lane arithmetic on a 32-bit element (one float, or a half2 pair).
+template <int PREC>
+struct FOps;
+
+template <>
+struct FOps<NRLDPC_F32> {
+  static constexpr int lanes = 1;
+  static constexpr uint32_t sign = 0x80000000u;
+  __device__ static uint32_t sat() { return 0x7F800000u; }  // +inf: the f32 fold identity
+  __device__ static uint32_t sub_clamp(uint32_t a, uint32_t b) {
+    return __float_as_uint(__fsub_rn(__uint_as_float(a), __uint_as_float(b)));
+  }
+  __device__ static uint32_t add_clamp(uint32_t a, uint32_t b) {
+    return __float_as_uint(__fadd_rn(__uint_as_float(a), __uint_as_float(b)));
+  }
+  __device__ static uint32_t absv(uint32_t a) { return a & 0x7FFFFFFFu; }
+  __device__ static uint32_t minv(uint32_t a, uint32_t b) {
+    return __float_as_uint(fminf(__uint_as_float(a), __uint_as_float(b)));
+  }
+  __device__ static uint32_t maxv(uint32_t a, uint32_t b) {
+    return __float_as_uint(fmaxf(__uint_as_float(a), __uint_as_float(b)));
+  }
+  __device__ static uint32_t mul(uint32_t a, uint32_t b) {
+    return __float_as_uint(__fmul_rn(__uint_as_float(a), __uint_as_float(b)));
+  }
+  __device__ static uint32_t neg_mask(uint32_t a) { return __uint_as_float(a) < 0.0f ? 0xFFFFFFFFu : 0u; }
+  __device__ static uint32_t eq_mask(uint32_t a, uint32_t b) {
+    return __uint_as_float(a) == __uint_as_float(b) ? 0xFFFFFFFFu : 0u;
+  }
+  __device__ static float lane_abs(uint32_t a, int) { return fabsf(__uint_as_float(a)); }
+  __device__ static bool lane_neg(uint32_t a, int) { return __uint_as_float(a) < 0.0f; }
+};
+
+template <>
+struct FOps<NRLDPC_F16> {
+  static constexpr int lanes = 2;
+  static constexpr uint32_t sign = 0x80008000u;
+  __device__ static uint32_t sat() { return 0x7BFF7BFFu; }  // 65504 (F16_SAT)
+  __device__ static half2 clamp(half2 x) {
+    return __hmin2(__hmax2(x, u2h(0xFBFFFBFFu)), u2h(0x7BFF7BFFu));  // np.clip(+-65504)
+  }
+  __device__ static uint32_t sub_clamp(uint32_t a, uint32_t b) { return h2u(clamp(__hsub2(u2h(a), u2h(b)))); }
+  __device__ static uint32_t add_clamp(uint32_t a, uint32_t b) { return h2u(clamp(__hadd2(u2h(a), u2h(b)))); }
+  __device__ static uint32_t absv(uint32_t a) { return a & 0x7FFF7FFFu; }
+  __device__ static uint32_t minv(uint32_t a, uint32_t b) { return h2u(__hmin2(u2h(a), u2h(b))); }
+  __device__ static uint32_t maxv(uint32_t a, uint32_t b) { return h2u(__hmax2(u2h(a), u2h(b))); }
+  __device__ static uint32_t mul(uint32_t a, uint32_t b) { return h2u(__hmul2(u2h(a), u2h(b))); }
+  __device__ static uint32_t neg_mask(uint32_t a) { return __hlt2_mask(u2h(a), u2h(0u)); }
+  __device__ static uint32_t eq_mask(uint32_t a, uint32_t b) { return __heq2_mask(u2h(a), u2h(b)); }
+  __device__ static float lane_abs(uint32_t a, int l) {
+    return fabsf(__half2float(l ? __high2half(u2h(a)) : __low2half(u2h(a))));
+  }
+  __device__ static bool lane_neg(uint32_t a, int l) {
+    return __half2float(l ? __high2half(u2h(a)) : __low2half(u2h(a))) < 0.0f;
+  }
+};
+
+struct FltState {
+  int synd[2];
+  float minabs[2];
+  int done[2];
+  uint32_t accept[2];
+};
+
+template <int PREC>
+__global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KParams p,
+                                                    const void* __restrict__ llr,
+                                                    uint32_t* __restrict__ ws, KOut o) {
+  using F = FOps<PREC>;
+  constexpr int LANES = F::lanes;
+  extern __shared__ __align__(16) uint8_t smem[];
+  CtaState* cta = reinterpret_cast<CtaState*>(smem);
+  FltState* gstate = reinterpret_cast<FltState*>(smem + 16);
+  const uint32_t data_off = (16u + (uint32_t)sizeof(FltState) * p.groups + 15u) & ~15u;
+
+  const int tid = threadIdx.x;
+  const bool st_ok = tid < p.groups * p.z;
+  const int g = st_ok ? tid / p.z : p.groups - 1;
+  const int z = st_ok ? tid - g * p.z : (tid - g * p.z) % p.z;
+  const long long gg = (long long)blockIdx.x * p.groups + g;  // global group index
+  const long long cw0 = gg * LANES;
+  const bool active = st_ok && cw0 < p.batch;
+  const uint32_t ZL = (uint32_t)p.z * 4u;
+  const uint32_t zl = (uint32_t)z * 4u;
+  const long long n_c = (long long)p.n_blocks * p.z;
+  uint8_t* Lg = smem + data_off + (uint32_t)g * p.l_bytes;
+  uint32_t* Mg = ws + gg * (long long)p.n_edges * p.z + z;  // edge e at Mg[e * Z]
+  FltState& gs = gstate[g];
+
+  if (tid == 0) {
+    const long long first = (long long)blockIdx.x * p.groups * LANES;
+    cta->n_done = 0;
+    cta->n_valid = (int)min(p.batch - first, (long long)p.groups * LANES);
+  }
+  if (st_ok && z == 0) {
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+      gs.synd[l] = 0;
+      gs.minabs[l] = __int_as_float(0x7F800000);
+      gs.done[l] = 0;
+      gs.accept[l] = 0;
+    }
+  }
+  bool lane_valid[2];
+  lane_valid[0] = active;
+  lane_valid[1] = active && LANES == 2 && cw0 + 1 < p.batch;
+
+  // load posteriors (decoder.py:286: astype to the engine dtype, done by the
+  // caller) and zero the messages of this group
+  if (st_ok) {
+    for (int c = 0; c < p.n_blocks; ++c) {
+      const long long n = (long long)c * p.z + z;
+      uint32_t v = 0;
+      if (PREC == NRLDPC_F32) {
+        if (lane_valid[0]) v = reinterpret_cast<const uint32_t*>(llr)[cw0 * n_c + n];
+      } else {
+        const uint16_t* h = reinterpret_cast<const uint16_t*>(llr);
+        const uint32_t lo = lane_valid[0] ? h[cw0 * n_c + n] : 0u;
+        const uint32_t hi = lane_valid[1] ? h[(cw0 + 1) * n_c + n] : 0u;
+        v = lo | (hi << 16);
+      }
+      *reinterpret_cast<uint32_t*>(Lg + (uint32_t)n * 4u) = v;
+    }
+    if (active)
+      for (int e = 0; e < p.n_edges; ++e) Mg[(long long)e * p.z] = 0u;
+  }
+  __syncthreads();
+
+  const uint32_t beta = p.beta_f;
+  for (int it = 1; it <= p.max_iter; ++it) {
+    for (int r = 0; r < p.rows; ++r) {
+      const int e0 = p.row_start[r];
+      const int w = p.row_start[r + 1] - e0;
+      uint32_t tsh[19], tcb[19];
+      load_row_tables<19>(p, p.tab_start[r], w, tsh, tcb);
+      uint32_t off[19], t[19], neg[19];
+      uint32_t m1 = F::sat(), m2 = F::sat(), S = 0;
+#pragma unroll
+      for (int j = 0; j < 19; ++j) {
+        if (j < w) {
+          off[j] = edge_offset(tsh[j], tcb[j], zl, ZL);
+          const uint32_t lv = *reinterpret_cast<const uint32_t*>(Lg + off[j]);
+          const uint32_t mv = Mg[(long long)(e0 + j) * p.z];
+          t[j] = F::sub_clamp(lv, mv);                 // decoder.py:300
+          const uint32_t a = F::absv(t[j]);
+          neg[j] = F::neg_mask(t[j]);                  // lvc < 0 (-0 is not negative)
+          m2 = F::minv(m2, F::maxv(m1, a));            // kernels.py:247-250
+          m1 = F::minv(m1, a);
+          S ^= neg[j];
+        }
+      }
+      const uint32_t b1 = F::mul(beta, m1), b2 = F::mul(beta, m2);  // dtype(beta) * m
+#pragma unroll
+      for (int j = 0; j < 19; ++j) {
+        if (j < w) {
+          const uint32_t eq = F::eq_mask(F::absv(t[j]), m1);        // the argmin edge (ties: m1 == m2)
+          const uint32_t mag = (eq & b2) | (~eq & b1);
+          const uint32_t out = mag ^ ((S ^ neg[j]) & F::sign);       // -mag flips the sign bit
+          if (active) {
+            Mg[(long long)(e0 + j) * p.z] = out;
+            *reinterpret_cast<uint32_t*>(Lg + off[j]) = F::add_clamp(t[j], out);  // decoder.py:318
+          }
+        }
+      }
+      __syncthreads();
+    }
+    const bool last = it == p.max_iter;
+    if (!(p.early_stop != NRLDPC_STOP_NONE || p.trace || last)) continue;
+
+    // end-of-iteration check (decoder.py:497-536)
+    if (active) {
+      int wc[2] = {0, 0};
+      for (int r = 0; r < p.rows; ++r) {
+        const int w = p.row_start[r + 1] - p.row_start[r];
+        uint32_t tsh[19], tcb[19];
+        load_row_tables<19>(p, p.tab_start[r], w, tsh, tcb);
+        uint32_t par = 0;
+#pragma unroll
+        for (int j = 0; j < 19; ++j)
+          if (j < w) par ^= F::neg_mask(*reinterpret_cast<const uint32_t*>(Lg + edge_offset(tsh[j], tcb[j], zl, ZL)));
+        if (LANES == 1) {
+          wc[0] += par >> 31;
+        } else {  // half2 masks: lane 0 in bits 0-15, lane 1 in bits 16-31
+          wc[0] += (par >> 15) & 1u;
+          wc[1] += par >> 31;
+        }
+      }
+      float ma[2] = {__int_as_float(0x7F800000), __int_as_float(0x7F800000)};
+      for (int c = 0; c < p.n_blocks; ++c) {
+        const uint32_t v = *reinterpret_cast<const uint32_t*>(Lg + (uint32_t)c * ZL + zl);
+#pragma unroll
+        for (int l = 0; l < LANES; ++l) ma[l] = fminf(ma[l], F::lane_abs(v, l));
+      }
+#pragma unroll
+      for (int l = 0; l < LANES; ++l) {
+        if (wc[l]) atomicAdd(&gs.synd[l], wc[l]);
+        atomicMin(reinterpret_cast<int*>(&gs.minabs[l]), __float_as_int(ma[l]));  // non-negative floats
+      }
+    }
+    __syncthreads();
+    int cand[2] = {0, 0};
+    if (active && p.early_stop != NRLDPC_STOP_NONE) {
+#pragma unroll
+      for (int l = 0; l < LANES; ++l)
+        cand[l] = lane_valid[l] && !gs.done[l] && gs.synd[l] == 0 && gs.minabs[l] > 0.0f;
+    }
+    if (p.early_stop == NRLDPC_STOP_CRC) {
+      if (active) {
+        const int K = p.k_b * p.z;
+#pragma unroll
+        for (int l = 0; l < LANES; ++l) {
+          if (!cand[l]) continue;
+          uint32_t acc = p.crc_tab ? 0u : 1u;
+          if (p.crc_tab)
+            for (int i = z; i < K; i += p.z) {
+              const uint32_t v = *reinterpret_cast<const uint32_t*>(Lg + (uint32_t)i * 4u);
+              if (F::lane_neg(v, l)) acc ^= __ldg(p.crc_tab + i);
+            }
+          if (acc) atomicXor(&gs.accept[l], acc);
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int l = 0; l < LANES; ++l) cand[l] = cand[l] && p.crc_tab != nullptr && gs.accept[l] == 0;
+    }
+    int fin[2] = {0, 0};
+    if (active && last) {
+#pragma unroll
+      for (int l = 0; l < LANES; ++l) fin[l] = lane_valid[l] && !gs.done[l] && !cand[l];
+    }
+    if (active) {
+      const int K = p.k_b * p.z;
+#pragma unroll
+      for (int l = 0; l < LANES; ++l) {
+        if (!(cand[l] || fin[l])) continue;
+        for (int wi = z; wi < p.words; wi += p.z) {
+          const int base = wi * 32;
+          const int nb = min(32, K - base);
+          uint32_t word = 0;
+          for (int i = 0; i < nb; ++i)
+            word |= (F::lane_neg(*reinterpret_cast<const uint32_t*>(Lg + (uint32_t)(base + i) * 4u), l) ? 1u : 0u) << i;
+          o.bits[(cw0 + l) * p.words + wi] = word;
+        }
+      }
+      if (z == 0) {
+#pragma unroll
+        for (int l = 0; l < LANES; ++l) {
+          if (!lane_valid[l]) continue;
+          const long long cw = cw0 + l;
+          const int wgt = gs.synd[l];
+          const float mar = gs.minabs[l];
+          if (p.trace) {
+            o.trace_w[cw * p.max_iter + (it - 1)] = wgt;
+            o.trace_m[cw * p.max_iter + (it - 1)] = mar;
+          }
+          if (cand[l]) {
+            o.iters[cw] = it;
+            o.synd[cw] = 0;
+            o.success[cw] = 1;
+            if (o.crc_ok) o.crc_ok[cw] = 1;
+          } else if (fin[l]) {
+            o.iters[cw] = p.max_iter;
+            o.synd[cw] = wgt;
+            o.success[cw] = (p.early_stop == NRLDPC_STOP_NONE && wgt == 0 && mar > 0.0f) ? 1 : 0;
+            if (o.crc_ok) o.crc_ok[cw] = 0;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (active && z == 0) {
+      int newly = 0;
+#pragma unroll
+      for (int l = 0; l < LANES; ++l) {
+        if (cand[l]) {
+          gs.done[l] = 1;
+          ++newly;
+        }
+        gs.synd[l] = 0;
+        gs.minabs[l] = __int_as_float(0x7F800000);
+        gs.accept[l] = 0;
+      }
+      if (newly) atomicAdd(&cta->n_done, newly);
+    }
+    __syncthreads();
+    if (__syncthreads_and(!p.trace && cta->n_done >= cta->n_valid)) break;
+  }
+}
+
+}  // namespace nr

@@ -64,6 +64,7 @@ struct alignas(16) KParams {
   alignas(16) uint32_t sh[NR_MAX_TAB];  // shift * LANES (bytes)
   alignas(16) uint32_t cb[NR_MAX_TAB];  // col * z * LANES (bytes)
   const uint32_t* crc_tab;          // crc mode: rem(x^(K-1-i+L), g), device memory
+  uint32_t beta_f;                  // float engines: dtype(beta) (f32 bits or half2)
   int beta_mode;                    // 1: half-arithmetic beta (beta_h, ndelta_h, c_h)
   uint32_t beta_h, ndelta_h, c_h;   // half2 constants of the arithmetic beta rule
   uint16_t lut[128];                // floor(beta*m) as half bits, m = 0..127

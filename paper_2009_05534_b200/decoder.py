@@ -102,6 +102,7 @@ class DecodeResult:
     crc_ok: np.ndarray | None = None
 
 
+_FLOAT_DTYPE = {Precision.F16: np.float16, Precision.F32: np.float32}
 _PREC_CODE = {Precision.INT8: _native.INT8, Precision.F16: _native.F16, Precision.F32: _native.F32}
 _STOP_CODE = {EarlyStop.SYNDROME: _native.STOP_SYNDROME, EarlyStop.CRC: _native.STOP_CRC,
               EarlyStop.NONE: _native.STOP_NONE}
@@ -260,9 +261,6 @@ def decode(llrs, bg, cfg: DecodeConfig, trace: list | None = None) -> DecodeResu
     (n_c,) or (B, n_c); results are host numpy arrays.
     """
     cfg = _coerce_cfg(cfg)
-    if cfg.precision is not Precision.INT8:
-        raise NotImplementedError(
-            f"precision {cfg.precision.value} has no sm_100a kernel yet (int8 only in this build)")
     if _is_torch(llrs) and llrs.is_cuda:
         return _decode_torch(llrs, bg, cfg, trace)
     arr = np.asarray(llrs)
@@ -271,10 +269,13 @@ def decode(llrs, bg, cfg: DecodeConfig, trace: list | None = None) -> DecodeResu
     if cfg.precision is Precision.INT8 and cfg.rho == 4 and arr.shape[0] % 4:
         raise ValueError("packed int8 decode needs a multiple of 4 codewords")
     rows_used = _rows_used(arr.shape[-1], bg)
-    wide = arr.astype(np.int32)  # decoder.py:286 (astype semantics)
-    if wide.size and np.abs(wide).max() > INT8_SAT:
-        raise ValueError("int8 LLR magnitudes must be at most 127")
-    host = np.ascontiguousarray(wide.astype(np.int8))
+    if cfg.precision is Precision.INT8:
+        wide = arr.astype(np.int32)  # decoder.py:286 (astype semantics)
+        if wide.size and np.abs(wide).max() > INT8_SAT:
+            raise ValueError("int8 LLR magnitudes must be at most 127")
+        host = np.ascontiguousarray(wide.astype(np.int8))
+    else:
+        host = np.ascontiguousarray(arr.astype(_FLOAT_DTYPE[cfg.precision]))
     import torch
     plan = get_plan(bg, rows_used, cfg)
     dev_in = torch.from_numpy(host).to(f"cuda:{plan.device}", non_blocking=False)
@@ -289,7 +290,9 @@ def _decode_torch(llrs, bg, cfg, trace):
         raise ValueError("packed int8 decode needs a multiple of 4 codewords")
     rows_used = _rows_used(int(x.shape[-1]), bg)
     import torch
-    if x.dtype != torch.int8:
+    if cfg.precision is not Precision.INT8:
+        x = x.to(torch.float16 if cfg.precision is Precision.F16 else torch.float32)
+    elif x.dtype != torch.int8:
         wide = x.to(torch.int32)
         if wide.numel() and int(wide.abs().max()) > INT8_SAT:
             raise ValueError("int8 LLR magnitudes must be at most 127")

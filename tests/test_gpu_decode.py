@@ -1,8 +1,9 @@
 """GPU parity: the sm_100a decoder (through the C ABI) against the reference's
 golden vectors and against the pinned C oracle at full BASELINE sizes.
 
-Bar: bit-exact bits, iterations, success, syndrome weight, crc_ok and trace
-(int8 fixed-point path).
+Bar: bit-exact bits, iterations, success, syndrome weight, crc_ok and trace,
+for the int8 fixed-point path and for the f16/f32 paths (IEEE round-to-nearest
+in the reference's operation order makes the float paths exact as well).
 """
 
 import numpy as np
@@ -17,7 +18,7 @@ from tests.golden_cases import load_cases, make_cfg
 
 pytestmark = pytest.mark.gpu
 
-INT8_CASES = sorted(n for n, c in load_cases()["cases"].items() if c.cfg["precision"] == "int8")
+ALL_CASES = sorted(load_cases()["cases"])
 
 
 def assert_same(res, ref_bits, ref_iters, ref_succ, ref_synd, ref_crc=None):
@@ -31,8 +32,8 @@ def assert_same(res, ref_bits, ref_iters, ref_succ, ref_synd, ref_crc=None):
         assert np.array_equal(res.crc_ok, ref_crc)
 
 
-@pytest.mark.parametrize("name", INT8_CASES)
-def test_golden_int8(cuda_ok, name):
+@pytest.mark.parametrize("name", ALL_CASES)
+def test_golden(cuda_ok, name):
     case = load_cases()["cases"][name]
     bg = nr.load_basegraph(case.bg, case.z)
     cfg = make_cfg(case, nr.DecodeConfig)
@@ -225,3 +226,30 @@ def test_crc_at_full_size_vs_oracle(cuda_ok):
     blocks = oracle.quantize_i8(nr.demap_llr(nr.bpsk_awgn(tx, sigma, rng), sigma), 384)
     res = _oracle_cmp(bg, 46, nr.DecodeConfig(max_iter=12, early_stop="crc"), blocks)
     assert not res.crc_ok[5] and res.crc_ok.sum() >= 4  # int8 at scale 8 converges for some
+
+
+@pytest.mark.parametrize("prec", ["f32", "f16"])
+def test_float_paths_vs_oracle(cuda_ok, prec):
+    """f32 (one codeword per thread) and f16 (two per half2) engines: exact."""
+    for bg_id, z, rows, b, stop in (("BG1", 384, 46, 6, "none"), ("BG2", 52, 42, 33, "syndrome"),
+                                    ("BG1", 7, 46, 17, "syndrome"), ("BG2", 384, 20, 5, "syndrome")):
+        bg = nr.load_basegraph(bg_id, z)
+        params = nr.code_params(bg, z, rows)
+        _, llr = noisy_llrs(bg, rows, 1.75, b, seed=(z, rows, 5))
+        blocks = nr.quantize(llr, nr.QuantConfig(mode=prec), params)
+        cfg = nr.DecodeConfig(precision=prec, max_iter=9, early_stop=stop)
+        _oracle_cmp(bg, rows, cfg, blocks, trace=True)
+
+
+def test_float_crc_vs_oracle(cuda_ok):
+    bg = nr.load_basegraph("BG2", 64)
+    params = nr.code_params(bg, 64, 42)
+    rng = np.random.default_rng(33)
+    msgs = np.stack([nr.crc_attach(rng.integers(0, 2, params.k - 24, dtype=np.uint8), k=params.k)
+                     for _ in range(12)])
+    tx = nr.encode_batch(msgs, bg, 64, 42)[:, 128:]
+    sigma = nr.ebn0_to_sigma(1.5, params.k / params.n_tx)
+    llr = nr.demap_llr(nr.bpsk_awgn(tx, sigma, rng), sigma)
+    for prec in ("f32", "f16"):
+        blocks = nr.quantize(llr, nr.QuantConfig(mode=prec), params)
+        _oracle_cmp(bg, 42, nr.DecodeConfig(precision=prec, max_iter=12, early_stop="crc"), blocks)
