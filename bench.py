@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
+    ap.add_argument("--chunks", type=int, default=4, help="e2e pipelining sub-batches")
     return ap.parse_args()
 
 
@@ -314,7 +315,7 @@ def run_ours(args):
         host_in.copy_(blocks0.cpu())
         hin = host_in.numpy()
         hout = plan.host_outputs(B, pinned=True)
-        chunks = 4
+        chunks = args.chunks
         for _ in range(max(1, args.warmup)):
             plan.decode_host(hin, chunks=chunks, out=hout)
         if world > 1:

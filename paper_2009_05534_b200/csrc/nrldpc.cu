@@ -124,6 +124,50 @@ __device__ __forceinline__ void msg_store(uint8_t* Mrow, uint32_t* mreg, int j, 
   }
 }
 
+// Two smallest of |t_0..t_{W-1}| capped at the fold identity 127
+// (kernels.py:246-257 folded from m1 = m2 = 127), as a pairwise tree: the
+// same min/max work as the sequential fold but ~log2(W) deep instead of ~2W,
+// so the scheduler can overlap it. Pairs give (lo, hi); two pairs merge as
+// lo = min(lo_a, lo_b), hi = min(max(lo_a, lo_b), hi_a, hi_b).
+template <int N>
+__device__ __forceinline__ void mm_merge_level(half2 (&lo)[N], half2 (&hi)[N]) {
+  if constexpr (N > 1) {
+    constexpr int M = (N + 1) / 2;
+    half2 nlo[M], nhi[M];
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) {
+      nlo[i] = __hmin2(lo[2 * i], lo[2 * i + 1]);
+      nhi[i] = __hmin2(__hmin2(__hmax2(lo[2 * i], lo[2 * i + 1]), hi[2 * i]), hi[2 * i + 1]);
+    }
+    if constexpr (N & 1) {
+      nlo[M - 1] = lo[N - 1];
+      nhi[M - 1] = hi[N - 1];
+    }
+    mm_merge_level<M>(nlo, nhi);
+    lo[0] = nlo[0];
+    hi[0] = nhi[0];
+  }
+}
+
+template <int W>
+__device__ __forceinline__ void two_smallest(const half2 (&t)[W], half2& m1, half2& m2) {
+  const half2 H127 = u2h(0x57F057F0u);
+  constexpr int P = (W + 1) / 2;
+  half2 lo[P], hi[P];
+#pragma unroll
+  for (int i = 0; i < W / 2; ++i) {
+    lo[i] = __hmin2(__habs2(t[2 * i]), __habs2(t[2 * i + 1]));
+    hi[i] = __hmax2(__habs2(t[2 * i]), __habs2(t[2 * i + 1]));
+  }
+  if constexpr (W & 1) {
+    lo[P - 1] = __habs2(t[W - 1]);
+    hi[P - 1] = H127;
+  }
+  mm_merge_level<P>(lo, hi);
+  m1 = __hmin2(lo[0], H127);
+  m2 = __hmin2(hi[0], H127);
+}
+
 // One layer (base row r) for thread (group, z): gather, min-sum check-node
 // update, scatter. decoder.py:295-320. t0 is the row's slot in the graph
 // tables; me0 is the row's first edge in this thread's shared-memory message
@@ -157,11 +201,20 @@ struct RowWork {
         const half2 lh = unpack_elem<LANES>(ld_elem<LANES>(Lg + off[j]), magic);
         const half2 mh = msg_load<LANES, REGMSG>(Mrow, mreg, j, j, magic);
         const half2 tj = __hsub2(lh, mh);           // exact: L - M
-        const half2 aj = __habs2(tj);
-        m2 = __hmin2(m2, __hmax2(m1, aj));          // kernels.py:247-250
-        m1 = __hmin2(m1, aj);
         S ^= h2u(tj);                               // sign product (bits 15/31)
         t[j] = tj;
+      }
+    }
+    if (w == MAXW) {
+      two_smallest<MAXW>(t, m1, m2);                // kernels.py:247-250, as a tree
+    } else {
+#pragma unroll
+      for (int j = 0; j < MAXW; ++j) {
+        if (j < w) {
+          const half2 aj = __habs2(t[j]);
+          m2 = __hmin2(m2, __hmax2(m1, aj));        // kernels.py:247-250
+          m1 = __hmin2(m1, aj);
+        }
       }
     }
   }
