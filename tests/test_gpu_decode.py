@@ -253,3 +253,24 @@ def test_float_crc_vs_oracle(cuda_ok):
     for prec in ("f32", "f16"):
         blocks = nr.quantize(llr, nr.QuantConfig(mode=prec), params)
         _oracle_cmp(bg, 42, nr.DecodeConfig(precision=prec, max_iter=12, early_stop="crc"), blocks)
+
+
+def test_mixed_batch_cuda_graph_matches_per_group(cuda_ok):
+    """Transport-block style mixed batch (several graphs/Z/rows in one CUDA
+    graph replay) == one decode per group."""
+    from paper_2009_05534_b200.mixed import Group, MixedBatchDecoder
+    cfg = nr.DecodeConfig(max_iter=8)
+    shapes = [("BG1", 384, 46, 6), ("BG1", 352, 8, 9), ("BG2", 13, 42, 33), ("BG2", 240, 20, 4),
+              ("BG1", 2, 46, 70)]
+    groups, data = [], []
+    for bg_id, z, rows, b in shapes:
+        bg = nr.load_basegraph(bg_id, z)
+        _, llr = noisy_llrs(bg, rows, 2.0, b, seed=(z, rows, 8))
+        groups.append(Group(bg, rows, b))
+        data.append(oracle.quantize_i8(llr, z))
+    mixed = MixedBatchDecoder(groups, cfg, streams=4)
+    for _ in range(2):  # second call replays the captured graph
+        results = mixed.decode(data)
+        for (bg_id, z, rows, b), res, blocks in zip(shapes, results, data):
+            ref = oracle.decode(blocks, nr.load_basegraph(bg_id, z), cfg)
+            assert_same(res, ref["bits"], ref["iterations"], ref["success"], ref["syndrome_weight"])
