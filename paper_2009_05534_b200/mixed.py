@@ -72,8 +72,9 @@ class MixedBatchDecoder:
 
     def decode(self, llrs: list) -> list[DecodeResult]:
         """Host arrays (or tensors) in, one DecodeResult per group out."""
+        import torch
         for x, src in zip(self.inputs, llrs):
-            x.copy_(src if hasattr(src, "device") else __import__("torch").from_numpy(np.asarray(src)))
+            x.copy_(src if isinstance(src, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(src)))
         self.replay()
         results = []
         for plan, out in zip(self.plans, self.outputs):
