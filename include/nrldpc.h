@@ -133,6 +133,19 @@ int nrldpc_decode_host(nrldpc_plan* plan, const void* llr_host, int64_t batch,
                        uint8_t* success, uint8_t* crc_ok, int chunks);
 
 /*
+ * Synthetic traffic on the GPU. nrldpc_encode: systematic
+ * encoding (codec.py:66-139), msgs (batch, K) bytes 0/1 -> codewords
+ * (batch, n_c) bytes 0/1, bit-exact. nrldpc_channel_awgn: BPSK + AWGN
+ * (Philox4x32-10, Box-Muller) + L = 2y/sigma^2 + int8 quantize with the 2Z
+ * punctured positions zeroed (channel.py:47-83); statistically equivalent to
+ * the reference's numpy draws, not draw-for-draw. Device pointers, async.
+ */
+int nrldpc_encode(const nrldpc_plan* plan, const uint8_t* msgs, int64_t batch, uint8_t* out,
+                  void* stream);
+int nrldpc_channel_awgn(const nrldpc_plan* plan, const uint8_t* bits, int64_t batch, double sigma,
+                        double scale, uint64_t seed, int8_t* out, void* stream);
+
+/*
  * Roofline denominator: measured half2 instruction throughput of this GPU
  * (lane-ops/s, a lane-op = one 32-bit lane of one SASS instruction = two
  * codeword-values for the half2 kernels). alu: HMNMX2 only (ALU pipe);

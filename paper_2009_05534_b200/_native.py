@@ -32,6 +32,8 @@ EXPORTS = (
     "nrldpc_demap_quantize",
     "nrldpc_decode",
     "nrldpc_decode_host",
+    "nrldpc_encode",
+    "nrldpc_channel_awgn",
     "nrldpc_launch_count",
     "nrldpc_alu_peak",
     "nrldpc_beta_rule",
@@ -78,6 +80,11 @@ def load() -> ctypes.CDLL:
     lib.nrldpc_decode.restype = c_int
     lib.nrldpc_decode_host.argtypes = [c_void_p, c_void_p, c_int64] + [c_void_p] * 5 + [c_int]
     lib.nrldpc_decode_host.restype = c_int
+    lib.nrldpc_encode.argtypes = [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]
+    lib.nrldpc_encode.restype = c_int
+    lib.nrldpc_channel_awgn.argtypes = [c_void_p, c_void_p, c_int64, c_double, c_double,
+                                        ctypes.c_uint64, c_void_p, c_void_p]
+    lib.nrldpc_channel_awgn.restype = c_int
     lib.nrldpc_alu_peak.argtypes = [c_int, c_void_p, c_void_p]
     lib.nrldpc_alu_peak.restype = c_int
     lib.nrldpc_beta_rule.argtypes = [c_double, c_void_p, c_void_p, c_void_p, c_void_p]

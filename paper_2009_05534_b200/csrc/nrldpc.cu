@@ -869,6 +869,7 @@ __global__ void __launch_bounds__(512) k_alu_peak(uint32_t* out, int iters, uint
 }  // namespace nr
 
 #include "nrldpc_float.cuh"
+#include "nrldpc_codec.cuh"
 
 // ---------------------------------------------------------------------------
 // Host side
@@ -890,6 +891,8 @@ struct nrldpc_plan {
   int early_stop = NRLDPC_STOP_SYNDROME;
   int crc_kind = NRLDPC_CRC24B;
   uint32_t* d_crc_tab = nullptr;  // device: rem(x^(K-1-i+L), g) for i < K (crc mode)
+  EncSched enc{};                 // systematic-encoder schedule (enc_ok)
+  bool enc_ok = false;
   double beta = 0.75;
   int max_iter = 20;
   int k_b = 0, z = 0, rows = 0, n_blocks = 0, n_edges = 0, maxw = 0;
@@ -1198,6 +1201,43 @@ int nrldpc_beta_rule(double beta, int* mode, float* beta_h, float* delta, float*
   return NRLDPC_OK;
 }
 
+int nrldpc_encode(const nrldpc_plan* plan, const uint8_t* msgs, int64_t batch, uint8_t* out,
+                  void* stream) {
+  g_launches = 0;
+  if (!plan) return fail(NRLDPC_EINVAL, "plan is NULL");
+  if (!plan->enc_ok) return fail(NRLDPC_EINVAL, "graph does not have the systematic-encoder structure");
+  if (batch < 0) return fail(NRLDPC_EINVAL, "batch must be non-negative");
+  if (batch == 0) return NRLDPC_OK;
+  if (!msgs || !out) return fail(NRLDPC_EINVAL, "NULL buffer");
+  NR_CUDA(cudaSetDevice(plan->device));
+  const int threads = (plan->z + 31) / 32 * 32;
+  const size_t smem = (size_t)(plan->n_blocks + 4) * plan->z;
+  k_encode<<<(unsigned)batch, threads, smem, (cudaStream_t)stream>>>(plan->base, plan->enc, msgs, batch, out);
+  ++g_launches;
+  NR_CUDA(cudaGetLastError());
+  return NRLDPC_OK;
+}
+
+int nrldpc_channel_awgn(const nrldpc_plan* plan, const uint8_t* bits, int64_t batch, double sigma,
+                        double scale, uint64_t seed, int8_t* out, void* stream) {
+  g_launches = 0;
+  if (!plan) return fail(NRLDPC_EINVAL, "plan is NULL");
+  if (!(sigma > 0.0)) return fail(NRLDPC_EINVAL, "sigma must be positive");
+  if (!(scale > 0.0)) return fail(NRLDPC_EINVAL, "scale must be positive");
+  if (batch < 0) return fail(NRLDPC_EINVAL, "batch must be non-negative");
+  if (batch == 0) return NRLDPC_OK;
+  if (!bits || !out) return fail(NRLDPC_EINVAL, "NULL buffer");
+  NR_CUDA(cudaSetDevice(plan->device));
+  const int n_c = plan->n_blocks * plan->z;
+  const long long total = batch * (long long)n_c;
+  const int grid = (int)std::min<long long>((total + 1023) / 1024, 148LL * 16);
+  k_channel_awgn<<<grid, 256, 0, (cudaStream_t)stream>>>(bits, batch, n_c, 2 * plan->z, sigma, scale,
+                                                         (unsigned long long)seed, out);
+  ++g_launches;
+  NR_CUDA(cudaGetLastError());
+  return NRLDPC_OK;
+}
+
 int nrldpc_alu_peak(int device, double* alu_lane_ops_per_s, double* mixed_lane_ops_per_s) {
   NR_CUDA(cudaSetDevice(device));
   int sms = 0;
@@ -1339,6 +1379,68 @@ int nrldpc_plan_create(int device, int k_b, int z, int rows_used, const int32_t*
     for (int r = 0; r <= rows_used && same; ++r)
       same = row_start[r] == (bg == 1 ? RowW<1>::e0[r] : RowW<2>::e0[r]);
     if (same) p->schedule = bg;
+  }
+  // systematic-encoder schedule (basegraph.py:175-207, codec.py:85-125)
+  {
+    const int p0 = k_b;
+    std::vector<int> core[4];
+    bool ok = true;
+    for (int r = 0; r < 4 && ok; ++r)
+      for (int e = row_start[r]; e < row_start[r + 1]; ++e)
+        if (cols[e] >= p0 && cols[e] < p0 + 4) core[cols[e] - p0].push_back(shifts[e]);
+        else if (cols[e] >= p0 + 4) ok = false;
+    for (int c = 1; c < 4 && ok; ++c) {
+      if (core[c].size() % 2) ok = false;
+      for (int v : core[c]) ok = ok && v == core[c][0];
+    }
+    // the shift value occurring an odd number of times at p0 (exactly one)
+    int odd = -1, n_odd = 0;
+    for (size_t i = 0; i < core[0].size(); ++i) {
+      bool first = true;
+      for (size_t k = 0; k < i; ++k) first = first && core[0][k] != core[0][i];
+      if (!first) continue;
+      int cnt = 0;
+      for (int u : core[0]) cnt += (u == core[0][i]);
+      if (cnt % 2) {
+        odd = core[0][i];
+        ++n_odd;
+      }
+    }
+    ok = ok && n_odd == 1;
+    EncSched es{};
+    es.css = odd;
+    bool known[4] = {true, false, false, false};
+    std::vector<int> pending = {0, 1, 2, 3};
+    while (ok && !pending.empty()) {
+      bool progressed = false;
+      for (size_t i = 0; i < pending.size(); ++i) {
+        const int r = pending[i];
+        int n_unknown = 0, uc = -1, us = 0;
+        for (int e = row_start[r]; e < row_start[r + 1]; ++e)
+          if (cols[e] >= p0 && !known[cols[e] - p0]) ++n_unknown, uc = cols[e], us = shifts[e];
+        if (n_unknown > 1) continue;
+        if (n_unknown == 1) {
+          es.row[es.nsteps] = r;
+          es.col[es.nsteps] = uc;
+          es.shift[es.nsteps] = us;
+          ++es.nsteps;
+          known[uc - p0] = true;
+        }
+        pending.erase(pending.begin() + i);
+        progressed = true;
+        break;
+      }
+      if (!progressed) ok = false;
+    }
+    for (int r = 4; r < rows_used && ok; ++r) {
+      int own = 0;
+      for (int e = row_start[r]; e < row_start[r + 1]; ++e)
+        if (cols[e] == p0 + r) own += shifts[e] == 0 ? 1 : 100;
+        else if (cols[e] >= p0 + 4) own += 100;
+      ok = own == 1;
+    }
+    p->enc = es;
+    p->enc_ok = ok;
   }
   if (early_stop == NRLDPC_STOP_CRC && k_b * z >= crc_len) {
     // rem(x^(K-1-i+L), g) for i = K-1 down to 0: start at x^L mod g = poly

@@ -274,3 +274,44 @@ def test_mixed_batch_cuda_graph_matches_per_group(cuda_ok):
         for (bg_id, z, rows, b), res, blocks in zip(shapes, results, data):
             ref = oracle.decode(blocks, nr.load_basegraph(bg_id, z), cfg)
             assert_same(res, ref["bits"], ref["iterations"], ref["success"], ref["syndrome_weight"])
+
+
+@pytest.mark.parametrize("bg_id,z,rows", [("BG1", 384, 46), ("BG2", 13, 42), ("BG1", 7, 9),
+                                          ("BG2", 240, 4), ("BG1", 2, 46)])
+def test_gpu_encoder_matches_host_encoder(cuda_ok, bg_id, z, rows):
+    from paper_2009_05534_b200 import sim
+    bg = nr.load_basegraph(bg_id, z)
+    plan = nr.get_plan(bg, rows, nr.DecodeConfig())
+    rng = np.random.default_rng(z)
+    msgs = rng.integers(0, 2, size=(19, bg.k_b * z), dtype=np.uint8)
+    got = sim.encode(torch.from_numpy(msgs).cuda(), plan).cpu().numpy()
+    assert np.array_equal(got, nr.encode_batch(msgs, bg, z, rows))   # codec.py:66-139
+
+
+def test_gpu_channel_statistics(cuda_ok):
+    """BPSK/AWGN/demap/quantize on the GPU: punctured zeros, right LLR moments."""
+    from paper_2009_05534_b200 import sim
+    bg = nr.load_basegraph("BG1", 384)
+    plan = nr.get_plan(bg, 46, nr.DecodeConfig())
+    bits = torch.randint(0, 2, (64, plan.n_c), dtype=torch.uint8, device="cuda")
+    sigma = 1.3
+    q = sim.channel(bits, plan, sigma, scale=1.0, seed=7).cpu().numpy().astype(np.float64)
+    b = bits.cpu().numpy()
+    assert not q[:, :768].any()
+    x, bb = q[:, 768:], b[:, 768:]
+    mean = 2.0 / sigma ** 2                       # E[L | b=0] = 2/sigma^2, Var = 4/sigma^2
+    assert abs(x[bb == 0].mean() - mean) < 0.02 and abs(x[bb == 1].mean() + mean) < 0.02
+    assert abs(x[bb == 0].std() - 2.0 / sigma) < 0.03
+    q2 = sim.channel(bits, plan, sigma, scale=1.0, seed=7).cpu().numpy()
+    assert np.array_equal(q, q2)                  # counter-based: reproducible
+
+
+def test_gpu_bler_sweep_monotone(cuda_ok):
+    from paper_2009_05534_b200 import sim
+    bg = nr.load_basegraph("BG2", 16)
+    pts = sim.bler_sweep(bg, 42, nr.DecodeConfig(max_iter=20), [float("inf"), 0.5, 2.0, 3.5],
+                         target_block_errors=100, max_codewords=4000, seed=808, batch=2000)
+    assert pts[0].block_errors == 0
+    for prev, nxt in zip(pts[1:], pts[2:]):
+        assert nxt.wilson()[0] <= prev.wilson()[1]
+    assert pts[1].bler > pts[3].bler
