@@ -122,6 +122,15 @@ int nrldpc_decode(nrldpc_plan* plan, const void* llr, int64_t batch,
                   float* trace_m, int32_t* status, void* stream);
 
 /*
+ * Flooding-schedule decode (decoder.py:337-365, 569-581): every row reads the
+ * previous iteration's posteriors, then L = sat(L_b + sum of messages).
+ * Same buffers and early-stop semantics as nrldpc_decode (device pointers).
+ */
+int nrldpc_decode_flooding(nrldpc_plan* plan, const void* llr, int64_t batch, uint32_t* bits,
+                           int32_t* iters, int32_t* synd, uint8_t* success, uint8_t* crc_ok,
+                           int32_t* trace_w, float* trace_m, void* stream);
+
+/*
  * Host-buffer entry point (the end-to-end path): llr_host (batch, n_c) and
  * outputs are HOST pointers. The library stages through pinned buffers and
  * pipelines H2D copy / decode / D2H copy over `chunks` sub-batches on its

@@ -165,6 +165,118 @@ static void layer_f16(const graph_t* g, h16* L, h16* M, h16 beta16, int r) {
   }
 }
 
+/* ---------------- flooding schedule (decoder.py:337-365) ----------------
+ * Check-node update of every row from the previous posteriors (messages are
+ * per row, updated in place after the row's gather), then
+ * L = sat(L_b + sum over the column's edges of roll(msg_e, s_e)), summed in
+ * int64 (int8) or float64 (floats) in row order, saturated once. */
+static void flood_i8(const graph_t* g, int32_t* L, const int32_t* Lb, int32_t* M, const int32_t* lut) {
+  const int Z = g->z;
+  for (int r = 0; r < g->rows; ++r) {
+    const int e0 = g->row_start[r], w = g->row_start[r + 1] - e0;
+    for (int z = 0; z < Z; ++z) {
+      int32_t t[32];
+      int32_t m1 = 127, m2 = 127, tag = -1, s = 0;
+      for (int j = 0; j < w; ++j) {
+        const int e = e0 + j;
+        t[j] = clamp127(L[g->cols[e] * Z + (z + g->shifts[e]) % Z] - M[e * Z + z]);
+        const int32_t mag = t[j] < 0 ? -t[j] : t[j];
+        const int y_wins = mag < m1;
+        const int32_t loser = y_wins ? m1 : mag;
+        m1 = y_wins ? mag : m1;
+        m2 = loser < m2 ? loser : m2;
+        tag = y_wins ? j : tag;
+        s ^= (t[j] < 0);
+      }
+      for (int j = 0; j < w; ++j) {
+        const int32_t mag = lut[(tag == j) ? m2 : m1];
+        M[(e0 + j) * Z + z] = (s ^ (t[j] < 0)) ? -mag : mag;
+      }
+    }
+  }
+  for (int c = 0; c < g->n_blocks; ++c)
+    for (int i = 0; i < Z; ++i) {
+      int64_t acc = Lb[c * Z + i];
+      for (int e = 0; e < g->n_edges; ++e)
+        if (g->cols[e] == c) acc += M[e * Z + ((i - g->shifts[e]) % Z + Z) % Z];
+      L[c * Z + i] = (int32_t)(acc < -127 ? -127 : (acc > 127 ? 127 : acc));
+    }
+}
+
+static void flood_f32(const graph_t* g, float* L, const float* Lb, float* M, float beta32) {
+  const int Z = g->z;
+  for (int r = 0; r < g->rows; ++r) {
+    const int e0 = g->row_start[r], w = g->row_start[r + 1] - e0;
+    for (int z = 0; z < Z; ++z) {
+      float t[32];
+      float m1 = INFINITY, m2 = INFINITY;
+      int tag = -1, s = 0;
+      for (int j = 0; j < w; ++j) {
+        const int e = e0 + j;
+        t[j] = L[g->cols[e] * Z + (z + g->shifts[e]) % Z] - M[e * Z + z];
+        const float mag = fabsf(t[j]);
+        const int y_wins = mag < m1;
+        const float loser = y_wins ? m1 : mag;
+        m1 = y_wins ? mag : m1;
+        m2 = loser < m2 ? loser : m2;
+        tag = y_wins ? j : tag;
+        s ^= (t[j] < 0.0f);
+      }
+      const float b1 = beta32 * m1, b2 = beta32 * m2;
+      for (int j = 0; j < w; ++j) {
+        const float mag = (tag == j) ? b2 : b1;
+        M[(e0 + j) * Z + z] = (s ^ (t[j] < 0.0f)) ? -mag : mag;
+      }
+    }
+  }
+  for (int c = 0; c < g->n_blocks; ++c)
+    for (int i = 0; i < Z; ++i) {
+      double acc = (double)Lb[c * Z + i];
+      for (int e = 0; e < g->n_edges; ++e)
+        if (g->cols[e] == c) acc += (double)M[e * Z + ((i - g->shifts[e]) % Z + Z) % Z];
+      L[c * Z + i] = (float)acc;
+    }
+}
+
+static void flood_f16(const graph_t* g, h16* L, const h16* Lb, h16* M, h16 beta16) {
+  const int Z = g->z;
+  const h16 sat = (h16)65504.0f;
+  for (int r = 0; r < g->rows; ++r) {
+    const int e0 = g->row_start[r], w = g->row_start[r + 1] - e0;
+    for (int z = 0; z < Z; ++z) {
+      h16 t[32];
+      h16 m1 = sat, m2 = sat;
+      int tag = -1, s = 0;
+      for (int j = 0; j < w; ++j) {
+        const int e = e0 + j;
+        h16 d = (h16)(L[g->cols[e] * Z + (z + g->shifts[e]) % Z] - M[e * Z + z]);
+        t[j] = clamp_h(d);
+        const h16 mag = t[j] < (h16)0.0f ? (h16)(-t[j]) : t[j];
+        const int y_wins = mag < m1;
+        const h16 loser = y_wins ? m1 : mag;
+        m1 = y_wins ? mag : m1;
+        m2 = loser < m2 ? loser : m2;
+        tag = y_wins ? j : tag;
+        s ^= (t[j] < (h16)0.0f);
+      }
+      const h16 b1 = (h16)(beta16 * m1), b2 = (h16)(beta16 * m2);
+      for (int j = 0; j < w; ++j) {
+        const h16 mag = (tag == j) ? b2 : b1;
+        M[(e0 + j) * Z + z] = (s ^ (t[j] < (h16)0.0f)) ? (h16)(-mag) : mag;
+      }
+    }
+  }
+  for (int c = 0; c < g->n_blocks; ++c)
+    for (int i = 0; i < Z; ++i) {
+      double acc = (double)Lb[c * Z + i];
+      for (int e = 0; e < g->n_edges; ++e)
+        if (g->cols[e] == c) acc += (double)M[e * Z + ((i - g->shifts[e]) % Z + Z) % Z];
+      if (acc < -65504.0) acc = -65504.0;
+      if (acc > 65504.0) acc = 65504.0;
+      L[c * Z + i] = (h16)acc; /* double -> half, one RNE rounding (astype) */
+    }
+}
+
 /* syndrome weight and min|L| of the current posteriors; sign test is v < 0 */
 #define DEF_CHECK(NAME, T, NEG, ABS)                                                \
   static void NAME(const graph_t* g, const T* L, int64_t* wgt, double* margin) {   \
@@ -210,7 +322,7 @@ typedef struct {
 } outs_t;
 
 static void decode_one(const graph_t* g, int prec, const void* llr_cw, int64_t b, const outs_t* o,
-                       void* Lbuf, void* Mbuf, uint8_t* hard) {
+                       void* Lbuf, void* Mbuf, uint8_t* hard, void* LBbuf, int flooding) {
   const int Z = g->z, K = g->k_b * Z, NC = g->n_blocks * Z, E = g->n_edges;
   int32_t lut[128];
   for (int m = 0; m < 128; ++m) lut[m] = (int32_t)floor(g->beta * (double)m);
@@ -228,16 +340,26 @@ static void decode_one(const graph_t* g, int prec, const void* llr_cw, int64_t b
     memcpy(Lbuf, llr_cw, sizeof(h16) * NC);
     memset(Mbuf, 0, sizeof(h16) * (size_t)E * Z);
   }
+  if (flooding) {
+    const size_t esz = prec == PREC_F16 ? 2 : 4;
+    memcpy(LBbuf, Lbuf, esz * (size_t)NC);
+  }
   const int tracing = o->trace_w != NULL;
   int done = 0;
   int64_t wgt = 0;
   double margin = 0.0;
   int it;
   for (it = 1; it <= g->max_iter; ++it) {
-    for (int r = 0; r < g->rows; ++r) {
-      if (prec == PREC_INT8) layer_i8(g, (int32_t*)Lbuf, (int32_t*)Mbuf, lut, r);
-      else if (prec == PREC_F32) layer_f32(g, (float*)Lbuf, (float*)Mbuf, beta32, r);
-      else layer_f16(g, (h16*)Lbuf, (h16*)Mbuf, beta16, r);
+    if (flooding) {
+      if (prec == PREC_INT8) flood_i8(g, (int32_t*)Lbuf, (const int32_t*)LBbuf, (int32_t*)Mbuf, lut);
+      else if (prec == PREC_F32) flood_f32(g, (float*)Lbuf, (const float*)LBbuf, (float*)Mbuf, beta32);
+      else flood_f16(g, (h16*)Lbuf, (const h16*)LBbuf, (h16*)Mbuf, beta16);
+    } else {
+      for (int r = 0; r < g->rows; ++r) {
+        if (prec == PREC_INT8) layer_i8(g, (int32_t*)Lbuf, (int32_t*)Mbuf, lut, r);
+        else if (prec == PREC_F32) layer_f32(g, (float*)Lbuf, (float*)Mbuf, beta32, r);
+        else layer_f16(g, (h16*)Lbuf, (h16*)Mbuf, beta16, r);
+      }
     }
     if (prec == PREC_INT8) check_i8(g, (const int32_t*)Lbuf, &wgt, &margin);
     else if (prec == PREC_F32) check_f32(g, (const float*)Lbuf, &wgt, &margin);
@@ -296,7 +418,7 @@ int oracle_decode(int precision, const void* llr, int64_t batch, int k_b, int z,
                   const int32_t* row_start, const int16_t* cols, const int16_t* shifts, double beta,
                   int max_iter, int early_stop, int crc_len, uint32_t crc_poly, uint8_t* bits,
                   int64_t* iters, int64_t* synd, uint8_t* success, uint8_t* crc_ok,
-                  int32_t* trace_w, double* trace_m, int n_threads) {
+                  int32_t* trace_w, double* trace_m, int n_threads, int flooding) {
   graph_t g = {k_b, z, rows_used, k_b + rows_used, row_start[rows_used], row_start, cols, shifts,
                beta, max_iter, early_stop, crc_len, crc_poly};
   outs_t o = {bits, iters, synd, success, crc_ok, trace_w, trace_m};
@@ -311,16 +433,19 @@ int oracle_decode(int precision, const void* llr, int64_t batch, int k_b, int z,
   {
     void* Lbuf = malloc(esz * (size_t)NC);
     void* Mbuf = malloc(esz * (size_t)g.n_edges * z);
+    void* LBbuf = malloc(esz * (size_t)NC);
     uint8_t* hard = (uint8_t*)malloc((size_t)k_b * z);
-    if (!Lbuf || !Mbuf || !hard) {
+    if (!Lbuf || !Mbuf || !hard || !LBbuf) {
       rc = -3;
     } else {
 #ifdef _OPENMP
 #pragma omp for schedule(dynamic, 1)
 #endif
       for (int64_t b = 0; b < batch; ++b)
-        decode_one(&g, precision, (const uint8_t*)llr + (size_t)b * NC * in_sz, b, &o, Lbuf, Mbuf, hard);
+        decode_one(&g, precision, (const uint8_t*)llr + (size_t)b * NC * in_sz, b, &o, Lbuf, Mbuf, hard,
+                   LBbuf, flooding);
     }
+    free(LBbuf);
     free(Lbuf);
     free(Mbuf);
     free(hard);

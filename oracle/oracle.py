@@ -41,7 +41,7 @@ def _load():
         lib.oracle_decode.argtypes = [
             ctypes.c_int, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp,
             ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_uint32,
-            vp, vp, vp, vp, vp, vp, vp, ctypes.c_int]
+            vp, vp, vp, vp, vp, vp, vp, ctypes.c_int, ctypes.c_int]
         lib.oracle_decode.restype = ctypes.c_int
         lib.oracle_quantize_i8.argtypes = [vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                            ctypes.c_double, vp]
@@ -64,7 +64,12 @@ def graph_tables(bg, rows_used: int):
     return (np.asarray(starts, np.int32), np.asarray(cols, np.int16), np.asarray(shifts, np.int16))
 
 
-def decode(llrs, bg, cfg, trace: list | None = None, threads: int = 0) -> dict:
+def decode_flooding(llrs, bg, cfg, trace: list | None = None, threads: int = 0) -> dict:
+    """Flooding schedule (decoder.py:337-365, 569-581)."""
+    return decode(llrs, bg, cfg, trace, threads, flooding=True)
+
+
+def decode(llrs, bg, cfg, trace: list | None = None, threads: int = 0, flooding: bool = False) -> dict:
     """Oracle decode. ``cfg`` is any DecodeConfig-like object (ours or the
     reference's). Returns a dict with bits/iterations/success/syndrome_weight/
     crc_ok and, when ``trace`` is a list, appends the reference-ordered trace."""
@@ -102,7 +107,7 @@ def decode(llrs, bg, cfg, trace: list | None = None, threads: int = 0) -> dict:
         shifts.ctypes.data, float(cfg.beta), int(cfg.max_iter), STOP[stop], crc_len, crc_poly,
         bits.ctypes.data, iters.ctypes.data, synd.ctypes.data, success.ctypes.data, crc_ok.ctypes.data,
         tw.ctypes.data if tw is not None else None, tm.ctypes.data if tm is not None else None,
-        int(threads or os.cpu_count() or 1))
+        int(threads or os.cpu_count() or 1), int(flooding))
     if rc:
         raise MemoryError("oracle workspace allocation failed")
     out = {"bits": bits, "iterations": iters, "success": success.astype(bool),

@@ -29,6 +29,7 @@ from .decoder import (
     Precision,
     Strategy,
     decode,
+    decode_flooding,
     get_plan,
     unpack_bits,
 )
@@ -37,6 +38,6 @@ __all__ = [
     "ALL_LIFTING_SIZES", "LIFTING_SETS", "BaseGraph", "CodeParams", "code_params", "edge_tables",
     "lifting_set_index", "load_basegraph", "QuantConfig", "bpsk_awgn", "bpsk_exact", "demap_llr",
     "ebn0_to_sigma", "quantize", "demap_quantize", "crc_attach", "crc_check", "encode_batch", "syndrome_weights",
-    "DecodeConfig", "DecodeResult", "EarlyStop", "Plan", "Precision", "Strategy", "decode",
+    "DecodeConfig", "DecodeResult", "EarlyStop", "Plan", "Precision", "Strategy", "decode", "decode_flooding",
     "get_plan", "unpack_bits",
 ]

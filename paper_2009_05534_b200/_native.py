@@ -32,6 +32,7 @@ EXPORTS = (
     "nrldpc_demap_quantize",
     "nrldpc_decode",
     "nrldpc_decode_host",
+    "nrldpc_decode_flooding",
     "nrldpc_encode",
     "nrldpc_channel_awgn",
     "nrldpc_launch_count",
@@ -80,6 +81,8 @@ def load() -> ctypes.CDLL:
     lib.nrldpc_decode.restype = c_int
     lib.nrldpc_decode_host.argtypes = [c_void_p, c_void_p, c_int64] + [c_void_p] * 5 + [c_int]
     lib.nrldpc_decode_host.restype = c_int
+    lib.nrldpc_decode_flooding.argtypes = [c_void_p, c_void_p, c_int64] + [c_void_p] * 8
+    lib.nrldpc_decode_flooding.restype = c_int
     lib.nrldpc_encode.argtypes = [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]
     lib.nrldpc_encode.restype = c_int
     lib.nrldpc_channel_awgn.argtypes = [c_void_p, c_void_p, c_int64, c_double, c_double,

@@ -870,6 +870,7 @@ __global__ void __launch_bounds__(512) k_alu_peak(uint32_t* out, int iters, uint
 
 #include "nrldpc_float.cuh"
 #include "nrldpc_codec.cuh"
+#include "nrldpc_flood.cuh"
 
 // ---------------------------------------------------------------------------
 // Host side
@@ -892,6 +893,7 @@ struct nrldpc_plan {
   int crc_kind = NRLDPC_CRC24B;
   uint32_t* d_crc_tab = nullptr;  // device: rem(x^(K-1-i+L), g) for i < K (crc mode)
   EncSched enc{};                 // systematic-encoder schedule (enc_ok)
+  FloodTables flood{};            // column-major edge lists (flooding schedule)
   bool enc_ok = false;
   double beta = 0.75;
   int max_iter = 20;
@@ -1201,6 +1203,54 @@ int nrldpc_beta_rule(double beta, int* mode, float* beta_h, float* delta, float*
   return NRLDPC_OK;
 }
 
+int nrldpc_decode_flooding(nrldpc_plan* plan, const void* llr, int64_t batch, uint32_t* bits,
+                           int32_t* iters, int32_t* synd, uint8_t* success, uint8_t* crc_ok,
+                           int32_t* trace_w, float* trace_m, void* stream) {
+  g_launches = 0;
+  if (!plan) return fail(NRLDPC_EINVAL, "plan is NULL");
+  if (batch < 0) return fail(NRLDPC_EINVAL, "batch must be non-negative");
+  if (batch == 0) return NRLDPC_OK;
+  if (!llr || !bits || !iters || !synd || !success) return fail(NRLDPC_EINVAL, "NULL buffer");
+  if ((trace_w == nullptr) != (trace_m == nullptr))
+    return fail(NRLDPC_EINVAL, "trace_w and trace_m must both be set or both NULL");
+  if (plan->early_stop == NRLDPC_STOP_CRC && !crc_ok)
+    return fail(NRLDPC_EINVAL, "crc mode needs a crc_ok buffer");
+  NR_CUDA(cudaSetDevice(plan->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  KParams kp = plan->base;
+  kp.batch = batch;
+  kp.trace = trace_w != nullptr;
+  if (plan->precision == NRLDPC_F32) {
+    const float bf = (float)plan->beta;
+    std::memcpy(&kp.beta_f, &bf, 4);
+  } else if (plan->precision == NRLDPC_F16) {
+    const __half bh = __double2half(plan->beta);
+    uint16_t u;
+    std::memcpy(&u, &bh, 2);
+    kp.beta_f = (uint32_t)u * 0x10001u;
+  }
+  const size_t n_c = (size_t)plan->n_blocks * plan->z;
+  const size_t smem = 2 * n_c * 4;
+  const int threads = (plan->z + 31) / 32 * 32;
+  void* ws = nullptr;
+  NR_CUDA(cudaMallocAsync(&ws, (size_t)batch * plan->n_edges * plan->z * 4, st));
+  KOut o{bits, iters, synd, success, crc_ok, trace_w, trace_m, nullptr};
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)batch, threads, smem, st>>>(kp, plan->flood, llr, ws, o);
+    return cudaGetLastError();
+  };
+  cudaError_t e = plan->precision == NRLDPC_INT8  ? go(k_decode_flood<NRLDPC_INT8>)
+                  : plan->precision == NRLDPC_F32 ? go(k_decode_flood<NRLDPC_F32>)
+                                                  : go(k_decode_flood<NRLDPC_F16>);
+  ++g_launches;
+  const cudaError_t f = cudaFreeAsync(ws, st);
+  if (e != cudaSuccess) return cuda_fail(e, "flooding decode launch");
+  if (f != cudaSuccess) return cuda_fail(f, "workspace free");
+  return NRLDPC_OK;
+}
+
 int nrldpc_encode(const nrldpc_plan* plan, const uint8_t* msgs, int64_t batch, uint8_t* out,
                   void* stream) {
   g_launches = 0;
@@ -1379,6 +1429,20 @@ int nrldpc_plan_create(int device, int k_b, int z, int rows_used, const int32_t*
     for (int r = 0; r <= rows_used && same; ++r)
       same = row_start[r] == (bg == 1 ? RowW<1>::e0[r] : RowW<2>::e0[r]);
     if (same) p->schedule = bg;
+  }
+  // flooding: per column, its edges in row order (decoder.py:362-364)
+  {
+    int k = 0;
+    for (int c = 0; c < n_blocks; ++c) {
+      p->flood.col_start[c] = (uint16_t)k;
+      for (int e = 0; e < n_edges; ++e)
+        if (cols[e] == c) {
+          p->flood.col_edge[k] = (uint16_t)e;
+          p->flood.col_shift[k] = (uint16_t)shifts[e];
+          ++k;
+        }
+    }
+    p->flood.col_start[n_blocks] = (uint16_t)k;
   }
   // systematic-encoder schedule (basegraph.py:175-207, codec.py:85-125)
   {

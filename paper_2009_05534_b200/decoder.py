@@ -159,6 +159,19 @@ class Plan:
             out["trace_m"] = torch.empty((batch, self.cfg.max_iter), dtype=torch.float32, device=dev)
         return out
 
+    def decode_flooding_device(self, llr, out: dict, stream=None) -> None:
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+        tw = out.get("trace_w")
+        tm = out.get("trace_m")
+        _native.check(_native.load().nrldpc_decode_flooding(
+            self.handle, llr.data_ptr(), int(llr.shape[0]),
+            out["bits"].data_ptr(), out["iters"].data_ptr(), out["synd"].data_ptr(),
+            out["success"].data_ptr(), out["crc_ok"].data_ptr(),
+            tw.data_ptr() if tw is not None else None, tm.data_ptr() if tm is not None else None,
+            stream))
+
     def decode_device(self, llr, out: dict, stream=None) -> None:
         """Asynchronous decode of a CUDA tensor (B, n_c) into ``out`` buffers."""
         import torch
@@ -301,7 +314,7 @@ def _decode_torch(llrs, bg, cfg, trace):
     return _run(plan, x.contiguous(), cfg, trace)
 
 
-def _run(plan: Plan, dev_in, cfg: DecodeConfig, trace) -> DecodeResult:
+def _run(plan: Plan, dev_in, cfg: DecodeConfig, trace, flooding: bool = False) -> DecodeResult:
     import torch
     batch = int(dev_in.shape[0])
     k = plan.k
@@ -310,7 +323,10 @@ def _run(plan: Plan, dev_in, cfg: DecodeConfig, trace) -> DecodeResult:
                             success=np.zeros(0, bool), syndrome_weight=np.zeros(0, np.int64),
                             crc_ok=np.zeros(0, bool) if cfg.early_stop is EarlyStop.CRC else None)
     out = plan.alloc_outputs(batch, trace=trace is not None)
-    plan.decode_device(dev_in, out)
+    if flooding:
+        plan.decode_flooding_device(dev_in, out)
+    else:
+        plan.decode_device(dev_in, out)
     host = {name: t.cpu().numpy() for name, t in out.items()}  # synchronizes
     if int(host["status"][0]):
         raise ValueError("int8 LLR magnitudes must be at most 127")
@@ -344,6 +360,42 @@ def _append_trace(trace: list, tw: np.ndarray, tm: np.ndarray, iterations: np.nd
         for it in range(1, last + 1):
             for b in members:
                 trace.append((b, it, int(tw[b, it - 1]), float(tm[b, it - 1])))
+
+
+def decode_flooding(llrs, bg, cfg: DecodeConfig, trace: list | None = None) -> DecodeResult:
+    """Flooding-schedule decode on the GPU (decoder.py:569-581): all rows
+    consume the previous iteration's posteriors. Same inputs/outputs as
+    ``decode``; the packed rho=4 engine is rejected as in the reference."""
+    cfg = _coerce_cfg(cfg)
+    if cfg.precision is Precision.INT8 and cfg.rho == 4:
+        raise ValueError("flooding decoding runs on the scalar path (rho < 4)")
+    import torch
+    if _is_torch(llrs) and llrs.is_cuda:
+        x = llrs.unsqueeze(0) if llrs.dim() == 1 else llrs
+        arr = None
+    else:
+        arr = np.asarray(llrs)
+        if arr.ndim == 1:
+            arr = arr[None, :]
+    n_c = int((x if arr is None else arr).shape[-1])
+    rows_used = _rows_used(n_c, bg)
+    if arr is not None:
+        if cfg.precision is Precision.INT8:
+            wide = arr.astype(np.int32)
+            if wide.size and np.abs(wide).max() > INT8_SAT:
+                raise ValueError("int8 LLR magnitudes must be at most 127")
+            arr = wide.astype(np.int8)
+        else:
+            arr = arr.astype(_FLOAT_DTYPE[cfg.precision])
+        plan = get_plan(bg, rows_used, cfg)
+        x = torch.from_numpy(np.ascontiguousarray(arr)).to(f"cuda:{plan.device}")
+    else:
+        if cfg.precision is Precision.INT8:
+            x = x.to(torch.int8)
+        else:
+            x = x.to(torch.float16 if cfg.precision is Precision.F16 else torch.float32)
+        plan = get_plan(bg, rows_used, cfg, device=x.device.index or 0)
+    return _run(plan, x.contiguous(), cfg, trace, flooding=True)
 
 
 def _coerce_cfg(cfg) -> DecodeConfig:

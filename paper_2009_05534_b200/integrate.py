@@ -23,6 +23,8 @@ _TARGETS = (
     ("ldpclab.decoder", "decode", _decoder.decode),
     ("ldpclab.harness", "decode", _decoder.decode),
     ("ldpclab", "decode", _decoder.decode),
+    ("ldpclab.decoder", "decode_flooding", _decoder.decode_flooding),
+    ("ldpclab", "decode_flooding", _decoder.decode_flooding),
     ("ldpclab.channel", "quantize", _channel.quantize),
     ("ldpclab.harness", "quantize", _channel.quantize),
     ("ldpclab", "quantize", _channel.quantize),

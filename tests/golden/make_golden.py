@@ -35,11 +35,12 @@ CASES = []
 
 def case(name, bg_id, z, rows, blocks, **cfg_kw):
     trace_on = cfg_kw.pop("trace", False)
+    flooding = cfg_kw.pop("flooding", False)
     cfg = rdec.DecodeConfig(**cfg_kw)
     bg = rbg.load_basegraph(bg_id, z)
     trace = [] if trace_on else None
-    res = rdec.decode(blocks, bg, cfg, trace)
-    meta = {"name": name, "bg": bg_id, "z": z, "rows": rows, "trace": trace_on,
+    res = (rdec.decode_flooding if flooding else rdec.decode)(blocks, bg, cfg, trace)
+    meta = {"name": name, "bg": bg_id, "z": z, "rows": rows, "trace": trace_on, "flooding": flooding,
             "cfg": {k: (v.value if hasattr(v, "value") else v) for k, v in cfg.__dict__.items()}}
     arrays = {
         "llr": np.asarray(blocks),
@@ -149,6 +150,21 @@ def main():
     case("bg2_z16_f16", "BG2", 16, 42, blk, precision="f16", max_iter=20)
     _, blk = make_noisy_blocks(g("BG1", 32), 46, 1.75, 8, seed=49, mode="f16")
     case("bg1_z32_f16_none", "BG1", 32, 46, blk, precision="f16", max_iter=10, early_stop="none")
+    # flooding schedule (decoder.py:337-365, 569-581)
+    _, blk = make_noisy_blocks(g("BG2", 16), 42, 2.5, 24, seed=29, mode="f32")
+    case("flood_bg2_z16_f32", "BG2", 16, 42, blk, precision="f32", max_iter=50, flooding=True)
+    case("flood_bg2_z16_f32_trace", "BG2", 16, 42, blk[:4], precision="f32", max_iter=8,
+         flooding=True, trace=True)
+    _, blk = make_noisy_blocks(g("BG2", 16), 42, 2.0, 24, seed=30)
+    case("flood_bg2_z16_i8", "BG2", 16, 42, blk, precision=I8, max_iter=20, flooding=True)
+    case("flood_bg2_z16_i8_none", "BG2", 16, 42, blk, precision=I8, max_iter=6, flooding=True,
+         early_stop="none")
+    _, blk = make_noisy_blocks(g("BG1", 24), 46, 2.0, 8, seed=31, mode="f16")
+    case("flood_bg1_z24_f16", "BG1", 24, 46, blk, precision="f16", max_iter=20, flooding=True)
+    _, blk = make_noisy_blocks(g("BG1", 104), 10, 3.0, 8, seed=32)
+    case("flood_bg1_z104_rows10_i8", "BG1", 104, 10, blk, precision=I8, max_iter=15, flooding=True)
+    blk = noise_free(g("BG2", 16), 42, 19, mode="f32")
+    case("flood_bg2_z16_noisefree", "BG2", 16, 42, blk, precision="f32", flooding=True)
     # config 4 shape: every lifting size, both graphs, 2 codewords each
     for bg_id in ("BG1", "BG2"):
         for z in rbg.ALL_LIFTING_SIZES:

@@ -20,6 +20,7 @@ class Case:
     rows: int
     trace: bool
     cfg: dict
+    flooding: bool
     arrays: dict = field(repr=False)
 
     @property
@@ -43,7 +44,8 @@ def load_cases() -> dict:
     for m in meta["cases"]:
         pre = m["name"] + "/"
         arrays = {k[len(pre):]: data[k] for k in data.files if k.startswith(pre)}
-        cases[m["name"]] = Case(m["name"], m["bg"], m["z"], m["rows"], m["trace"], m["cfg"], arrays)
+        cases[m["name"]] = Case(m["name"], m["bg"], m["z"], m["rows"], m["trace"], m["cfg"],
+                                m.get("flooding", False), arrays)
     quant = {k.split("/", 1)[1]: data[k] for k in data.files if k.startswith("quant/")}
     return {"cases": cases, "quant": quant}
 

@@ -38,7 +38,7 @@ def test_golden(cuda_ok, name):
     bg = nr.load_basegraph(case.bg, case.z)
     cfg = make_cfg(case, nr.DecodeConfig)
     trace = [] if case.trace else None
-    res = nr.decode(case.llr, bg, cfg, trace)
+    res = (nr.decode_flooding if case.flooding else nr.decode)(case.llr, bg, cfg, trace)
     crc = case.arrays["crc_ok"].astype(bool) if "crc_ok" in case.arrays else None
     assert_same(res, case.bits(), case.arrays["iterations"], case.arrays["success"].astype(bool),
                 case.arrays["syndrome_weight"], crc)
@@ -315,3 +315,45 @@ def test_gpu_bler_sweep_monotone(cuda_ok):
     for prev, nxt in zip(pts[1:], pts[2:]):
         assert nxt.wilson()[0] <= prev.wilson()[1]
     assert pts[1].bler > pts[3].bler
+
+
+@pytest.mark.parametrize("prec", ["int8", "f32", "f16"])
+def test_flooding_vs_oracle(cuda_ok, prec):
+    for bg_id, z, rows, b in (("BG1", 384, 46, 4), ("BG2", 52, 42, 20), ("BG1", 5, 12, 9)):
+        bg = nr.load_basegraph(bg_id, z)
+        params = nr.code_params(bg, z, rows)
+        _, llr = noisy_llrs(bg, rows, 2.0, b, seed=(z, 77))
+        blocks = nr.quantize(llr, nr.QuantConfig(mode=prec), params)
+        cfg = nr.DecodeConfig(precision=prec, max_iter=12)
+        tr_ref, tr = [], []
+        ref = oracle.decode_flooding(blocks, bg, cfg, tr_ref)
+        res = nr.decode_flooding(blocks, bg, cfg, tr)
+        assert_same(res, ref["bits"], ref["iterations"], ref["success"], ref["syndrome_weight"])
+        assert tr == tr_ref
+
+
+def test_flooding_rejects_packed(cuda_ok):
+    bg = nr.load_basegraph("BG2", 16)
+    with pytest.raises(ValueError, match="rho < 4"):
+        nr.decode_flooding(np.zeros((4, 832), np.int8), bg, nr.DecodeConfig(rho=4))
+
+
+def test_acceptance_layered_needs_fewer_iterations_than_flooding(cuda_ok):
+    """Reference acceptance criterion 7 (tests/test_acceptance.py:174-199):
+    BG2 Z=52 at 3 dB, f32, max 60: both >= 99% success and layered mean
+    iterations <= 0.65 x flooding, here on 2000 codewords decoded on the GPU."""
+    bg = nr.load_basegraph("BG2", 52)
+    params = nr.code_params(bg, 52, 42)
+    cfg = nr.DecodeConfig(precision="f32", max_iter=60)
+    lay_it, flo_it, lay_ok, flo_ok = [], [], 0, 0
+    for start in range(0, 2000, 500):
+        _, llr = noisy_llrs(bg, 42, 3.0, 500, seed=(700, start))
+        blocks = nr.quantize(llr, nr.QuantConfig(mode="f32"), params)
+        lay = nr.decode(blocks, bg, cfg)
+        flo = nr.decode_flooding(blocks, bg, cfg)
+        lay_it += lay.iterations.tolist()
+        flo_it += flo.iterations.tolist()
+        lay_ok += int(lay.success.sum())
+        flo_ok += int(flo.success.sum())
+    assert lay_ok >= 0.99 * 2000 and flo_ok >= 0.99 * 2000
+    assert np.mean(lay_it) <= 0.65 * np.mean(flo_it)

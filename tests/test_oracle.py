@@ -21,7 +21,7 @@ def test_oracle_matches_reference_golden(name):
     bg = load_basegraph(case.bg, case.z)
     cfg = make_cfg(case, DecodeConfig)
     trace = [] if case.trace else None
-    got = oracle.decode(case.llr, bg, cfg, trace, threads=4)
+    got = oracle.decode(case.llr, bg, cfg, trace, threads=4, flooding=case.flooding)
     assert np.array_equal(got["bits"], case.bits())
     assert np.array_equal(got["iterations"], case.arrays["iterations"])
     assert np.array_equal(got["success"], case.arrays["success"].astype(bool))
