@@ -67,6 +67,12 @@ struct CtaState {
 constexpr int kLutBytes = 256;
 constexpr int kCtaBytes = 16;
 
+// k_decode_i8's shared layout: LUT, CTA state, group states, then per group
+// L and messages from this 16-aligned offset
+__host__ __device__ constexpr uint32_t data_offset(int groups) {
+  return (kLutBytes + kCtaBytes + (uint32_t)sizeof(GroupState) * groups + 15u) & ~15u;
+}
+
 // (z + s) mod Z for one edge, as a byte offset into the group's L array.
 __device__ __forceinline__ uint32_t edge_offset(uint32_t shift, uint32_t colbase, uint32_t zl, uint32_t ZL) {
   uint32_t a = zl + shift;
@@ -173,7 +179,9 @@ __device__ __forceinline__ void two_smallest(const half2 (&t)[W], half2& m1, hal
 // tables; me0 is the row's first edge in this thread's shared-memory message
 // row. Split in two phases so that column-disjoint rows can be interleaved
 // in one basic block (process_rows2).
-template <int MAXW, int LANES, bool REGMSG>
+// ABS: the graph table's column bases are absolute shared-window addresses
+// (single-group CTAs); otherwise byte offsets from the group's L array.
+template <int MAXW, int LANES, bool REGMSG, bool ABS = false>
 struct RowWork {
   uint32_t off[MAXW];
   half2 t[MAXW];
@@ -198,7 +206,8 @@ struct RowWork {
     for (int j = 0; j < MAXW; ++j) {
       if (j < w) {
         off[j] = edge_offset(tsh[j], tcb[j], zl, ZL);
-        const half2 lh = unpack_elem<LANES>(ld_elem<LANES>(Lg + off[j]), magic);
+        const uint32_t raw = ABS ? lds_elem<LANES>(off[j]) : ld_elem<LANES>(Lg + off[j]);
+        const half2 lh = unpack_elem<LANES>(raw, magic);
         const half2 mh = msg_load<LANES, REGMSG>(Mrow, mreg, j, j, magic);
         const half2 tj = __hsub2(lh, mh);           // exact: L - M
         S ^= h2u(tj);                               // sign product (bits 15/31)
@@ -253,24 +262,29 @@ struct RowWork {
         // m1 == m2), else 1: |t| - m1 is a non-negative integer, saturated.
         const half2 x = __hsub2_sat(__habs2(t[j]), m1);
         const half2 mag = __hfma2(x, dd, b2s);       // +-b1 or +-b2
-        // L' = sign(t) * min(|clamp t| + mag', 127) == clamp127(t + out), using
-        // min(|t|,127) + mag' = min(|t| + mag', 127 + mag')
-        const half2 y = __hmin2(__hmin2(__hadd2(__habs2(t[j]), mag), __hadd2(mag, H127)), H127);
+        // L' = clamp127(clamp127(t) + out) with clamp127(t) = sign(t)*a,
+        // a = min(|t|,127), out = sign(t)*mag':  L' = sign(t)*min(a + mag', 127)
+        // (a + mag' >= -127, so the lower clamp never binds). The two mins are
+        // full-rate ALU ops; the FP16 pipe is the busier one in this phase.
+        const half2 a = __hmin2(__habs2(t[j]), H127);
+        const half2 y = __hmin2(__hadd2(a, mag), H127);
         const half2 sg = u2h((h2u(t[j]) & 0x80008000u) | one);
-        st_elem_if<LANES>(Lg + off[j], pack_elem<LANES>(__hfma2(y, sg, H1152)), st_ok);
+        const uint32_t lnew = pack_elem<LANES>(__hfma2(y, sg, H1152));
+        if constexpr (ABS) sts_elem_if<LANES>(off[j], lnew, st_ok);
+        else st_elem_if<LANES>(Lg + off[j], lnew, st_ok);
         msg_store<LANES, REGMSG>(Mrow, mreg, j, j, __hfma2(mag, sg, H1152), st_ok);
       }
     }
   }
 };
 
-template <int MAXW, int LANES, bool REGMSG>
+template <int MAXW, int LANES, bool REGMSG, bool ABS = false>
 __device__ __forceinline__ void process_row(const KParams& p, const int t0, const int me0, const int w,
                                             uint32_t zl, uint32_t ZL, uint8_t* __restrict__ Lg,
                                             uint8_t* __restrict__ Mz, uint32_t* mreg,
                                             const uint16_t* __restrict__ lut, uint32_t magic,
                                             uint32_t one, bool st_ok) {
-  RowWork<MAXW, LANES, REGMSG> r;
+  RowWork<MAXW, LANES, REGMSG, ABS> r;
   r.gather(p, t0, me0, w, zl, ZL, Lg, Mz, mreg, magic);
   if (p.beta_mode) r.beta_arith(p, one);
   else r.beta_lut(lut, one);
@@ -279,14 +293,14 @@ __device__ __forceinline__ void process_row(const KParams& p, const int t0, cons
 
 // Two consecutive column-disjoint rows as one basic block: no barrier between
 // them is needed and the scheduler interleaves their independent chains.
-template <int WA, int WB, int LANES>
+template <int WA, int WB, int LANES, bool ABS = false>
 __device__ __forceinline__ void process_rows2(const KParams& p, int t0a, int me0a, int t0b, int me0b,
                                               uint32_t zl, uint32_t ZL, uint8_t* __restrict__ Lg,
                                               uint8_t* __restrict__ Mz, uint32_t* mreg,
                                               const uint16_t* __restrict__ lut, uint32_t magic,
                                               uint32_t one, bool st_ok) {
-  RowWork<WA, LANES, false> a;
-  RowWork<WB, LANES, false> b;
+  RowWork<WA, LANES, false, ABS> a;
+  RowWork<WB, LANES, false, ABS> b;
   a.gather(p, t0a, me0a, WA, zl, ZL, Lg, Mz, mreg, magic);
   b.gather(p, t0b, me0b, WB, zl, ZL, Lg, Mz, mreg, magic);
   if (p.beta_mode) {
@@ -302,7 +316,7 @@ __device__ __forceinline__ void process_rows2(const KParams& p, int t0a, int me0
 
 // Syndrome weight (decoder.py:323-329) and min|L| (decoder.py:480-483) over
 // the thread's check rows / columns.
-template <int MAXW, int LANES>
+template <int MAXW, int LANES, bool ABS = false>
 __device__ __forceinline__ void row_parity(const KParams& p, const int t0, const int w, uint32_t zl,
                                            uint32_t ZL, const uint8_t* __restrict__ Lg, int& wa,
                                            int& wb) {
@@ -311,7 +325,10 @@ __device__ __forceinline__ void row_parity(const KParams& p, const int t0, const
   uint32_t x = 0;
 #pragma unroll
   for (int j = 0; j < MAXW; ++j) {
-    if (j < w) x ^= ld_elem<LANES>(Lg + edge_offset(tsh[j], tcb[j], zl, ZL));
+    if (j < w) {
+      const uint32_t a = edge_offset(tsh[j], tcb[j], zl, ZL);
+      x ^= ABS ? lds_elem<LANES>(a) : ld_elem<LANES>(Lg + a);
+    }
   }
   // bit 7 of a stored byte is 1 for a non-negative value
   if (w & 1) x ^= 0x8080u;
@@ -463,7 +480,7 @@ struct RegMsg {
   }
 };
 
-template <int BG, int MAXW, int LANES, int NREG>
+template <int BG, int MAXW, int LANES, int NREG, bool ABS>
 __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c, RegMsg<NREG>& rm) {
   if constexpr (BG == 0) {
     for (int r = 0; r < p.rows; ++r) {
@@ -477,19 +494,19 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
     if constexpr (NREG > 0) {
 #pragma unroll 1
       for (int r = 0; r < RegMsg<NREG>::nq; r += 2) {
-        process_row<19, LANES, true>(p, 20 * r, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, rm.q[0], c.lut, c.magic,
+        process_row<19, LANES, true, ABS>(p, 20 * r, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, rm.q[0], c.lut, c.magic,
                                      c.one, c.st_ok);
         __syncthreads();
-        process_row<19, LANES, true>(p, 20 * r + 20, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, rm.q[1], c.lut,
+        process_row<19, LANES, true, ABS>(p, 20 * r + 20, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, rm.q[1], c.lut,
                                      c.magic, c.one, c.st_ok);
         rm.rotate2();
         __syncthreads();
       }
       if constexpr (NREG == 6) {
-        process_row<3, LANES, true>(p, 80, 0, 3, c.zl, c.ZL, c.Lg, c.Mz, rm.r4, c.lut, c.magic, c.one,
+        process_row<3, LANES, true, ABS>(p, 80, 0, 3, c.zl, c.ZL, c.Lg, c.Mz, rm.r4, c.lut, c.magic, c.one,
                                     c.st_ok);
         __syncthreads();
-        process_row<8, LANES, true>(p, 84, 0, 8, c.zl, c.ZL, c.Lg, c.Mz, rm.r5, c.lut, c.magic, c.one,
+        process_row<8, LANES, true, ABS>(p, 84, 0, 8, c.zl, c.ZL, c.Lg, c.Mz, rm.r5, c.lut, c.magic, c.one,
                                     c.st_ok);
         __syncthreads();
       }
@@ -511,7 +528,7 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
         const int wb = (int)(nd.x >> 16);
         const int me0b = (int)(nd.y & 0xFFFFu);
         const bool fused = dispatch_pair<BG>(w, wb, [&](auto WA, auto WB) {
-          process_rows2<decltype(WA)::value, decltype(WB)::value, LANES>(
+          process_rows2<decltype(WA)::value, decltype(WB)::value, LANES, ABS>(
               p, t0, me0, t0b, me0b, c.zl, c.ZL, c.Lg, c.Mz, rm.r4, c.lut, c.magic, c.one, c.st_ok);
         });
         if (fused) {
@@ -523,7 +540,7 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
         }
       }
       dispatch_w<BG>(w, [&](auto W) {
-        process_row<decltype(W)::value, LANES, false>(p, t0, me0, decltype(W)::value, c.zl, c.ZL, c.Lg,
+        process_row<decltype(W)::value, LANES, false, ABS>(p, t0, me0, decltype(W)::value, c.zl, c.ZL, c.Lg,
                                                       c.Mz, rm.r4, c.lut, c.magic, c.one, c.st_ok);
       });
       // consecutive column-disjoint rows form one layer: the next row reads
@@ -533,7 +550,7 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
   }
 }
 
-template <int BG, int MAXW, int LANES>
+template <int BG, int MAXW, int LANES, bool ABS>
 __device__ __forceinline__ void local_check(const KParams& p, uint32_t zl, uint32_t ZL,
                                             const uint8_t* __restrict__ Lg, int* wcnt, int* mabs) {
   int wa = 0, wb = 0;
@@ -548,7 +565,7 @@ __device__ __forceinline__ void local_check(const KParams& p, uint32_t zl, uint3
       const int e0 = p.row_start[r];
       const int t0 = p.tab_start[r];
       dispatch_w<BG>(p.row_start[r + 1] - e0, [&](auto W) {
-        row_parity<decltype(W)::value, LANES>(p, t0, decltype(W)::value, zl, ZL, Lg, wa, wb);
+        row_parity<decltype(W)::value, LANES, ABS>(p, t0, decltype(W)::value, zl, ZL, Lg, wa, wb);
       });
     }
   }
@@ -604,15 +621,16 @@ __device__ __forceinline__ uint32_t crc_partial(const KParams& p, const uint8_t*
 // Threads beyond G*Z (warp padding) shadow the last group's z = tid - (G-1)*Z
 // clamp but never store, so the layer loop runs warp-uniform and the graph
 // tables stay in uniform registers.
-template <int BG, int MAXW, int LANES, int NREG>
+template <int BG, int MAXW, int LANES, int NREG, bool ABS>
 __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_constant__ KParams p,
                                                                    const int8_t* __restrict__ llr, KOut o) {
   static_assert(NREG == 0 || (BG == 1 && LANES == 2), "register messages: BG1 pairs only");
+  static_assert(!ABS || BG != 0, "absolute addressing: compile-time schedules only");
   extern __shared__ __align__(16) uint8_t smem[];
   uint16_t* lut = reinterpret_cast<uint16_t*>(smem);
   CtaState* cta = reinterpret_cast<CtaState*>(smem + kLutBytes);
   GroupState* gstate = reinterpret_cast<GroupState*>(smem + kLutBytes + kCtaBytes);
-  const uint32_t data_off = (kLutBytes + kCtaBytes + (uint32_t)sizeof(GroupState) * p.groups + 15u) & ~15u;
+  const uint32_t data_off = data_offset(p.groups);
 
   const int tid = threadIdx.x;
   const bool st_ok = tid < p.groups * p.z;           // not a padding thread
@@ -626,6 +644,11 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
   uint8_t* Lg = smem + data_off + (uint32_t)g * (p.l_bytes + p.m_bytes);
   uint8_t* Mz = Lg + p.l_bytes + (uint32_t)z * p.m_stride;
   GroupState& gs = gstate[g];
+  if constexpr (ABS) {
+    // the host folded the L array's shared-window address into the graph
+    // table (one group per CTA); a different window layout is a hard error
+    if ((uint32_t)__cvta_generic_to_shared(Lg) != p.abs_base) __trap();
+  }
 
   for (int i = tid; i < 128; i += blockDim.x) lut[i] = p.lut[i];
   if (tid == 0) {
@@ -711,14 +734,14 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
   RegMsg<NREG> rm;
   rm.init();
   for (int it = 1; it <= p.max_iter; ++it) {
-    one_iteration<BG, MAXW, LANES, NREG>(p, rc, rm);
+    one_iteration<BG, MAXW, LANES, NREG, ABS>(p, rc, rm);
     const bool last = it == p.max_iter;
     if (!(p.early_stop != NRLDPC_STOP_NONE || p.trace || last)) continue;
 
     // ---- end-of-iteration check (decoder.py:497-536) ----
     {
       int wc[2], ma[2];
-      local_check<BG, MAXW, LANES>(p, zl, ZL, Lg, wc, ma);
+      local_check<BG, MAXW, LANES, ABS>(p, zl, ZL, Lg, wc, ma);
       if (active) {
 #pragma unroll
         for (int l = 0; l < LANES; ++l) {
@@ -883,6 +906,7 @@ struct Shape {
   int threads = 32;
   size_t smem = 0;
   int occ = 0;      // resident CTAs per SM (0: not queried yet)
+  bool abs = false; // kp.cb holds absolute shared-window addresses
   KParams kp{};
 };
 
@@ -922,17 +946,21 @@ size_t padded_edges(int n_edges, int lanes) {
   return e;
 }
 
+// dynamic shared memory's offset in the CTA's shared window (sm_90+ reserve
+// 1 KB per CTA; no static __shared__ in k_decode_i8, no clusters)
+constexpr uint32_t kSmemWindowBase = 0x400;
+
 size_t smem_for(int groups, size_t l_bytes, size_t m_bytes) {
   return kLutBytes + kCtaBytes + sizeof(GroupState) * groups + 16 + groups * (l_bytes + m_bytes);
 }
 
 // Launch (or, with llr == nullptr, only prepare: set the smem attribute and
 // query occupancy) one decode kernel instance for `sh`.
-template <int BG, int MAXW, int LANES, int NREG = 0>
+template <int BG, int MAXW, int LANES, int NREG = 0, bool ABS = false>
 cudaError_t launch_i8(Shape& sh, int device, const int8_t* llr, long long batch, const KOut& o,
                       cudaStream_t st) {
   static bool attr_done[64] = {};
-  auto kern = k_decode_i8<BG, MAXW, LANES, NREG>;
+  auto kern = k_decode_i8<BG, MAXW, LANES, NREG, ABS>;
   if (!attr_done[device & 63]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (e != cudaSuccess) return e;
@@ -1117,9 +1145,14 @@ Shape choose_shape(const nrldpc_plan* p, int max_lanes) {
   }
   sh.kp.magic = 0x64646464u;
   sh.kp.one = 0x3C003C00u;
+  // single-group register-message shapes address L absolutely: the table
+  // holds column base + the L array's shared-window address (the dynamic
+  // window starts after the 1 KB system reservation; the kernel verifies)
+  sh.kp.abs_base = (nreg > 0 && best_g == 1) ? kSmemWindowBase + data_offset(1) : 0u;
+  sh.abs = sh.kp.abs_base != 0;
   for (int t = 0; t < NR_MAX_TAB; ++t) {
     sh.kp.sh[t] = p->base.sh[t] * lanes;
-    sh.kp.cb[t] = p->base.cb[t] * (uint32_t)p->z * lanes;
+    sh.kp.cb[t] = p->base.cb[t] * (uint32_t)p->z * lanes + sh.kp.abs_base;
   }
   return sh;
 }
@@ -1134,9 +1167,10 @@ static cudaError_t launch_shape(const nrldpc_plan* plan, Shape& sh, const int8_t
     case 1:
       if (!two) return launch_i8<1, 19, 1>(sh, dev, in, batch, o, st);
       if (sh.nreg == 0) return launch_i8<1, 19, 2>(sh, dev, in, batch, o, st);
-      if (sh.nreg == 2) return launch_i8<1, 19, 2, 2>(sh, dev, in, batch, o, st);
-      if (sh.nreg == 4) return launch_i8<1, 19, 2, 4>(sh, dev, in, batch, o, st);
-      return launch_i8<1, 19, 2, 6>(sh, dev, in, batch, o, st);
+      if (!sh.abs) return cudaErrorInvalidConfiguration;
+      if (sh.nreg == 2) return launch_i8<1, 19, 2, 2, true>(sh, dev, in, batch, o, st);
+      if (sh.nreg == 4) return launch_i8<1, 19, 2, 4, true>(sh, dev, in, batch, o, st);
+      return launch_i8<1, 19, 2, 6, true>(sh, dev, in, batch, o, st);
     case 2:
       return two ? launch_i8<2, 10, 2>(sh, dev, in, batch, o, st) : launch_i8<2, 10, 1>(sh, dev, in, batch, o, st);
     default:

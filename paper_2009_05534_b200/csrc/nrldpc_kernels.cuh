@@ -54,6 +54,7 @@ struct alignas(16) KParams {
   int e_reg;         // edges whose messages live in registers (rows < nreg)
   uint32_t magic;    // 0x64646464: PRMT filler byte (half exponent of 1024)
   uint32_t one;      // 0x3C003C00: half2 {1.0, 1.0}
+  uint32_t abs_base; // nonzero: cb holds shared-window addresses, L starts here
   uint16_t row_start[NR_MAX_ROWS + 1];  // first edge of each row (message offsets)
   uint16_t tab_start[NR_MAX_ROWS + 1];  // row's first slot in sh/cb (multiple of 4)
   uint8_t bar_after[NR_MAX_ROWS];       // 0: next row is column-disjoint from this layer
@@ -62,7 +63,7 @@ struct alignas(16) KParams {
   // per-edge graph tables, each row padded to a multiple of 4 slots so a row
   // loads them with 128-bit uniform constant loads
   alignas(16) uint32_t sh[NR_MAX_TAB];  // shift * LANES (bytes)
-  alignas(16) uint32_t cb[NR_MAX_TAB];  // col * z * LANES (bytes)
+  alignas(16) uint32_t cb[NR_MAX_TAB];  // col * z * LANES (bytes) [+ abs_base]
   const uint32_t* crc_tab;          // crc mode: rem(x^(K-1-i+L), g), device memory
   uint32_t beta_f;                  // float engines: dtype(beta) (f32 bits or half2)
   int beta_mode;                    // 1: half-arithmetic beta (beta_h, ndelta_h, c_h)
@@ -122,6 +123,30 @@ __device__ __forceinline__ void st_elem(uint8_t* p, uint32_t v) {
 template <int LANES>
 __device__ __forceinline__ void st_elem_if(uint8_t* p, uint32_t v, bool ok) {
   const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+  if (LANES == 2)
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.u16 [%0], %1; }" ::"r"(a), "h"((uint16_t)v),
+                 "r"((uint32_t)ok));
+  else
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.u8 [%0], %1; }" ::"r"(a), "h"((uint16_t)v),
+                 "r"((uint32_t)ok));
+}
+
+// The same accesses on absolute shared-window addresses. With the graph
+// table already holding (column base + window base), ptxas folds the add into
+// the load/store as [R + UR] and the per-edge address costs two instructions.
+// volatile keeps NVVM from moving the loads across barriers.
+template <int LANES>
+__device__ __forceinline__ uint32_t lds_elem(uint32_t a) {
+  uint16_t v;
+  if (LANES == 2)
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  else
+    asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+
+template <int LANES>
+__device__ __forceinline__ void sts_elem_if(uint32_t a, uint32_t v, bool ok) {
   if (LANES == 2)
     asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.u16 [%0], %1; }" ::"r"(a), "h"((uint16_t)v),
                  "r"((uint32_t)ok));
