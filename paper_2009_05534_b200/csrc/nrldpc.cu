@@ -80,12 +80,13 @@ __device__ __forceinline__ uint32_t edge_offset(uint32_t shift, uint32_t colbase
   return a + colbase;
 }
 
-// A row's shift/column tables (t0 is 4-aligned): 128-bit uniform loads.
+// A row's shift/column tables (tb = byte offset of its first slot, a
+// multiple of 16): 128-bit uniform loads.
 template <int MAXW>
-__device__ __forceinline__ void load_row_tables(const KParams& p, int t0, int w, uint32_t (&sh)[MAXW],
+__device__ __forceinline__ void load_row_tables(const KParams& p, uint32_t tb, int w, uint32_t (&sh)[MAXW],
                                                 uint32_t (&cb)[MAXW]) {
-  const uint4* S = reinterpret_cast<const uint4*>(p.sh) + (t0 >> 2);
-  const uint4* C = reinterpret_cast<const uint4*>(p.cb) + (t0 >> 2);
+  const uint4* S = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(p.sh) + tb);
+  const uint4* C = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(p.cb) + tb);
 #pragma unroll
   for (int k = 0; k < (MAXW + 3) / 4; ++k) {
     if (4 * k < w) {
@@ -191,14 +192,16 @@ struct RowWork {
   int w;
 
   // phase 1: gather L and the old messages, t = L - M, fold (m1, m2, S)
-  __device__ __forceinline__ void gather(const KParams& p, const int t0, const int me0, const int w_,
+  // tb: byte offset of the row's table slots; mb: byte offset of its first
+  // message in this thread's shared-memory message row
+  __device__ __forceinline__ void gather(const KParams& p, const uint32_t tb, const uint32_t mb, const int w_,
                                          uint32_t zl, uint32_t ZL, const uint8_t* __restrict__ Lg,
                                          uint8_t* __restrict__ Mz, const uint32_t* mreg, uint32_t magic) {
     const half2 H127 = u2h(0x57F057F0u);
     w = w_;
-    Mrow = Mz + me0 * LANES;
+    Mrow = Mz + mb;
     uint32_t tsh[MAXW], tcb[MAXW];
-    load_row_tables<MAXW>(p, t0, w, tsh, tcb);
+    load_row_tables<MAXW>(p, tb, w, tsh, tcb);
     m1 = H127;
     m2 = H127;
     S = 0;
@@ -279,13 +282,13 @@ struct RowWork {
 };
 
 template <int MAXW, int LANES, bool REGMSG, bool ABS = false>
-__device__ __forceinline__ void process_row(const KParams& p, const int t0, const int me0, const int w,
+__device__ __forceinline__ void process_row(const KParams& p, const uint32_t tb, const uint32_t mb, const int w,
                                             uint32_t zl, uint32_t ZL, uint8_t* __restrict__ Lg,
                                             uint8_t* __restrict__ Mz, uint32_t* mreg,
                                             const uint16_t* __restrict__ lut, uint32_t magic,
                                             uint32_t one, bool st_ok) {
   RowWork<MAXW, LANES, REGMSG, ABS> r;
-  r.gather(p, t0, me0, w, zl, ZL, Lg, Mz, mreg, magic);
+  r.gather(p, tb, mb, w, zl, ZL, Lg, Mz, mreg, magic);
   if (p.beta_mode) r.beta_arith(p, one);
   else r.beta_lut(lut, one);
   r.scatter(Lg, mreg, one, st_ok);
@@ -294,15 +297,16 @@ __device__ __forceinline__ void process_row(const KParams& p, const int t0, cons
 // Two consecutive column-disjoint rows as one basic block: no barrier between
 // them is needed and the scheduler interleaves their independent chains.
 template <int WA, int WB, int LANES, bool ABS = false>
-__device__ __forceinline__ void process_rows2(const KParams& p, int t0a, int me0a, int t0b, int me0b,
+__device__ __forceinline__ void process_rows2(const KParams& p, uint32_t tba, uint32_t mba, uint32_t tbb,
+                                              uint32_t mbb,
                                               uint32_t zl, uint32_t ZL, uint8_t* __restrict__ Lg,
                                               uint8_t* __restrict__ Mz, uint32_t* mreg,
                                               const uint16_t* __restrict__ lut, uint32_t magic,
                                               uint32_t one, bool st_ok) {
   RowWork<WA, LANES, false, ABS> a;
   RowWork<WB, LANES, false, ABS> b;
-  a.gather(p, t0a, me0a, WA, zl, ZL, Lg, Mz, mreg, magic);
-  b.gather(p, t0b, me0b, WB, zl, ZL, Lg, Mz, mreg, magic);
+  a.gather(p, tba, mba, WA, zl, ZL, Lg, Mz, mreg, magic);
+  b.gather(p, tbb, mbb, WB, zl, ZL, Lg, Mz, mreg, magic);
   if (p.beta_mode) {
     a.beta_arith(p, one);
     b.beta_arith(p, one);
@@ -317,11 +321,11 @@ __device__ __forceinline__ void process_rows2(const KParams& p, int t0a, int me0
 // Syndrome weight (decoder.py:323-329) and min|L| (decoder.py:480-483) over
 // the thread's check rows / columns.
 template <int MAXW, int LANES, bool ABS = false>
-__device__ __forceinline__ void row_parity(const KParams& p, const int t0, const int w, uint32_t zl,
+__device__ __forceinline__ void row_parity(const KParams& p, const uint32_t tb, const int w, uint32_t zl,
                                            uint32_t ZL, const uint8_t* __restrict__ Lg, int& wa,
                                            int& wb) {
   uint32_t tsh[MAXW], tcb[MAXW];
-  load_row_tables<MAXW>(p, t0, w, tsh, tcb);
+  load_row_tables<MAXW>(p, tb, w, tsh, tcb);
   uint32_t x = 0;
 #pragma unroll
   for (int j = 0; j < MAXW; ++j) {
@@ -407,27 +411,25 @@ __device__ __forceinline__ void dispatch_w(int w, F&& f) {
   }
 }
 
-// Fused pairs of column-disjoint rows that occur in the base graphs
-// (BG1 rows 16..45, BG2 rows 11..41); returns false if (wa, wb) has no
-// compiled body (the caller then runs the two rows back to back).
+// Layer units of the compile-time schedules: code = wa | wb << 8 (wb = 0: a
+// single row). Fused pairs are the column-disjoint consecutive rows that
+// occur in the base graphs (BG1 rows 16..45, BG2 rows 11..41); the host
+// (build_units) fuses exactly these. The chain is ordered by how often each
+// unit occurs per iteration of the full graph.
 template <int BG, typename F>
-__device__ __forceinline__ bool dispatch_pair(int wa, int wb, F&& f) {
+__device__ __forceinline__ void dispatch_unit(uint32_t code, F&& f) {
+  const int c = (int)code;
+#define NR_U(a, b) else if (weq(c, (a) | ((b) << 8))) f(IC<a>{}, IC<b>{})
   if constexpr (BG == 1) {
-    if (weq(wa, 5) && weq(wb, 5)) f(IC<5>{}, IC<5>{});
-    else if (weq(wa, 6) && weq(wb, 6)) f(IC<6>{}, IC<6>{});
-    else if (weq(wa, 5) && weq(wb, 4)) f(IC<5>{}, IC<4>{});
-    else if (weq(wa, 4) && weq(wb, 5)) f(IC<4>{}, IC<5>{});
-    else if (weq(wa, 6) && weq(wb, 5)) f(IC<6>{}, IC<5>{});
-    else return false;
+    if (false) {}
+    NR_U(5, 5); NR_U(5, 4); NR_U(7, 0); NR_U(6, 6); NR_U(6, 0); NR_U(4, 5); NR_U(9, 0); NR_U(6, 5);
+    NR_U(10, 0); NR_U(8, 0); NR_U(19, 0); NR_U(3, 0); NR_U(5, 0); NR_U(4, 0);
   } else {
-    if (weq(wa, 4) && weq(wb, 4)) f(IC<4>{}, IC<4>{});
-    else if (weq(wa, 4) && weq(wb, 3)) f(IC<4>{}, IC<3>{});
-    else if (weq(wa, 5) && weq(wb, 3)) f(IC<5>{}, IC<3>{});
-    else if (weq(wa, 5) && weq(wb, 4)) f(IC<5>{}, IC<4>{});
-    else if (weq(wa, 3) && weq(wb, 4)) f(IC<3>{}, IC<4>{});
-    else return false;
+    if (false) {}
+    NR_U(4, 4); NR_U(4, 0); NR_U(5, 0); NR_U(4, 3); NR_U(6, 0); NR_U(5, 4); NR_U(5, 3); NR_U(8, 0);
+    NR_U(10, 0); NR_U(3, 4); NR_U(3, 0);
   }
-  return true;
+#undef NR_U
 }
 
 // Register-resident messages (BG1 pairs at the largest Z, see choose_shape):
@@ -485,7 +487,7 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
   if constexpr (BG == 0) {
     for (int r = 0; r < p.rows; ++r) {
       const int e0 = p.row_start[r];
-      process_row<MAXW, LANES, false>(p, p.tab_start[r], e0, p.row_start[r + 1] - e0, c.zl, c.ZL, c.Lg, c.Mz,
+      process_row<MAXW, LANES, false>(p, 4u * p.tab_start[r], (uint32_t)e0 * LANES, p.row_start[r + 1] - e0, c.zl, c.ZL, c.Lg, c.Mz,
                                       rm.r4, c.lut, c.magic, c.one, c.st_ok);
       if (p.bar_after[r]) __syncthreads();
     }
@@ -494,58 +496,49 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
     if constexpr (NREG > 0) {
 #pragma unroll 1
       for (int r = 0; r < RegMsg<NREG>::nq; r += 2) {
-        process_row<19, LANES, true, ABS>(p, 20 * r, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, rm.q[0], c.lut, c.magic,
+        process_row<19, LANES, true, ABS>(p, 80u * r, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, rm.q[0], c.lut, c.magic,
                                      c.one, c.st_ok);
         __syncthreads();
-        process_row<19, LANES, true, ABS>(p, 20 * r + 20, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, rm.q[1], c.lut,
+        process_row<19, LANES, true, ABS>(p, 80u * r + 80u, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, rm.q[1], c.lut,
                                      c.magic, c.one, c.st_ok);
         rm.rotate2();
         __syncthreads();
       }
       if constexpr (NREG == 6) {
-        process_row<3, LANES, true, ABS>(p, 80, 0, 3, c.zl, c.ZL, c.Lg, c.Mz, rm.r4, c.lut, c.magic, c.one,
+        process_row<3, LANES, true, ABS>(p, 320u, 0, 3, c.zl, c.ZL, c.Lg, c.Mz, rm.r4, c.lut, c.magic, c.one,
                                     c.st_ok);
         __syncthreads();
-        process_row<8, LANES, true, ABS>(p, 84, 0, 8, c.zl, c.ZL, c.Lg, c.Mz, rm.r5, c.lut, c.magic, c.one,
+        process_row<8, LANES, true, ABS>(p, 336u, 0, 8, c.zl, c.ZL, c.Lg, c.Mz, rm.r5, c.lut, c.magic, c.one,
                                     c.st_ok);
         __syncthreads();
       }
       r0 = NREG;
     }
-    // row descriptors are loaded one row ahead so the dispatch for the next
-    // row does not wait on the constant cache after the barrier
-    uint2 nd = p.rowdesc[r0];
+    // The remaining rows run as host-built units (a single row, or two
+    // consecutive column-disjoint rows fused into one basic block) with
+    // precomputed byte offsets; each unit's descriptor is loaded one unit
+    // ahead so the dispatch after a barrier does not wait on the constant
+    // cache.
+    uint4 na = p.unit_a[0];
+    uint2 nb = p.unit_b[0];
 #pragma unroll 1
-    for (int r = r0; r < p.rows; ++r) {
-      const uint2 d = nd;
-      nd = p.rowdesc[r + 1];
-      const int t0 = (int)(d.x & 0xFFFFu);
-      const int w = (int)(d.x >> 16);
-      const int me0 = (int)(d.y & 0xFFFFu);
-      if ((d.y >> 16) == 0 && r + 1 < p.rows) {
-        // rows r and r+1 share no column: one fused body when compiled
-        const int t0b = (int)(nd.x & 0xFFFFu);
-        const int wb = (int)(nd.x >> 16);
-        const int me0b = (int)(nd.y & 0xFFFFu);
-        const bool fused = dispatch_pair<BG>(w, wb, [&](auto WA, auto WB) {
-          process_rows2<decltype(WA)::value, decltype(WB)::value, LANES, ABS>(
-              p, t0, me0, t0b, me0b, c.zl, c.ZL, c.Lg, c.Mz, rm.r4, c.lut, c.magic, c.one, c.st_ok);
-        });
-        if (fused) {
-          ++r;
-          const uint2 d2 = nd;
-          nd = p.rowdesc[r + 1];
-          if (d2.y >> 16) __syncthreads();
-          continue;
-        }
-      }
-      dispatch_w<BG>(w, [&](auto W) {
-        process_row<decltype(W)::value, LANES, false, ABS>(p, t0, me0, decltype(W)::value, c.zl, c.ZL, c.Lg,
-                                                      c.Mz, rm.r4, c.lut, c.magic, c.one, c.st_ok);
+    for (int u = 0; u < p.n_units; ++u) {
+      const uint4 A = na;
+      const uint2 B = nb;
+      na = p.unit_a[u + 1];
+      nb = p.unit_b[u + 1];
+      dispatch_unit<BG>(A.x, [&](auto WA, auto WB) {
+        constexpr int wa = decltype(WA)::value, wb = decltype(WB)::value;
+        if constexpr (wb == 0)
+          process_row<wa, LANES, false, ABS>(p, A.z, A.w, wa, c.zl, c.ZL, c.Lg, c.Mz, rm.r4, c.lut, c.magic,
+                                             c.one, c.st_ok);
+        else
+          process_rows2<wa, wb, LANES, ABS>(p, A.z, A.w, B.x, B.y, c.zl, c.ZL, c.Lg, c.Mz, rm.r4, c.lut,
+                                            c.magic, c.one, c.st_ok);
       });
-      // consecutive column-disjoint rows form one layer: the next row reads
+      // consecutive column-disjoint rows form one layer: the next unit reads
       // no column this one wrote, so warps may run ahead into it
-      if (d.y >> 16) __syncthreads();
+      if (A.y) __syncthreads();
     }
   }
 }
@@ -557,7 +550,7 @@ __device__ __forceinline__ void local_check(const KParams& p, uint32_t zl, uint3
   if constexpr (BG == 0) {
     for (int r = 0; r < p.rows; ++r) {
       const int e0 = p.row_start[r];
-      row_parity<MAXW, LANES>(p, p.tab_start[r], p.row_start[r + 1] - e0, zl, ZL, Lg, wa, wb);
+      row_parity<MAXW, LANES>(p, 4u * p.tab_start[r], p.row_start[r + 1] - e0, zl, ZL, Lg, wa, wb);
     }
   } else {
 #pragma unroll 1
@@ -565,7 +558,7 @@ __device__ __forceinline__ void local_check(const KParams& p, uint32_t zl, uint3
       const int e0 = p.row_start[r];
       const int t0 = p.tab_start[r];
       dispatch_w<BG>(p.row_start[r + 1] - e0, [&](auto W) {
-        row_parity<decltype(W)::value, LANES, ABS>(p, t0, decltype(W)::value, zl, ZL, Lg, wa, wb);
+        row_parity<decltype(W)::value, LANES, ABS>(p, 4u * t0, decltype(W)::value, zl, ZL, Lg, wa, wb);
       });
     }
   }
@@ -1085,6 +1078,44 @@ Shape choose_shape_float(const nrldpc_plan* p) {
   return sh;
 }
 
+// Host side of dispatch_unit: which consecutive column-disjoint row pairs
+// have a fused body.
+bool fused_pair(int schedule, int wa, int wb) {
+  static const int bg1[][2] = {{5, 5}, {5, 4}, {6, 6}, {4, 5}, {6, 5}};
+  static const int bg2[][2] = {{4, 4}, {4, 3}, {5, 4}, {5, 3}, {3, 4}};
+  const auto& t = schedule == 1 ? bg1 : bg2;
+  for (const auto& q : t)
+    if (q[0] == wa && q[1] == wb) return true;
+  return false;
+}
+
+// Layer units for rows nreg.. of a BG1/BG2 kernel (see KParams::unit_a).
+void build_units(const nrldpc_plan* p, int nreg, int e_reg, int lanes, KParams& kp) {
+  const KParams& b = p->base;
+  int n = 0;
+  for (int r = nreg; r < p->rows;) {
+    const int wa = b.row_start[r + 1] - b.row_start[r];
+    const uint32_t ta = 4u * b.tab_start[r], ma = (uint32_t)(b.row_start[r] - e_reg) * lanes;
+    if (p->schedule != 0 && !b.bar_after[r] && r + 1 < p->rows) {
+      const int wb = b.row_start[r + 2] - b.row_start[r + 1];
+      if (fused_pair(p->schedule, wa, wb)) {
+        kp.unit_a[n] = make_uint4((uint32_t)(wa | wb << 8), b.bar_after[r + 1], ta, ma);
+        kp.unit_b[n] = make_uint2(4u * b.tab_start[r + 1], (uint32_t)(b.row_start[r + 1] - e_reg) * lanes);
+        ++n;
+        r += 2;
+        continue;
+      }
+    }
+    kp.unit_a[n] = make_uint4((uint32_t)wa, b.bar_after[r], ta, ma);
+    kp.unit_b[n] = make_uint2(0, 0);
+    ++n;
+    r += 1;
+  }
+  kp.n_units = n;
+  kp.unit_a[n] = make_uint4(0, 0, 0, 0);
+  kp.unit_b[n] = make_uint2(0, 0);
+}
+
 Shape choose_shape(const nrldpc_plan* p, int max_lanes) {
   const size_t smem_max = 232448;
   const size_t n_pos = (size_t)p->n_blocks * p->z;
@@ -1137,12 +1168,7 @@ Shape choose_shape(const nrldpc_plan* p, int max_lanes) {
   sh.kp.m_bytes = (uint32_t)mb;
   sh.kp.m_stride = (uint32_t)(e_pad * lanes);
   sh.kp.e_reg = e_reg;
-  for (int r = 0; r < p->rows; ++r) {
-    const int e0 = p->base.row_start[r];
-    const int w = p->base.row_start[r + 1] - e0;
-    sh.kp.rowdesc[r] = make_uint2((uint32_t)p->base.tab_start[r] | ((uint32_t)w << 16),
-                                  (uint32_t)(e0 - e_reg) | ((uint32_t)p->base.bar_after[r] << 16));
-  }
+  build_units(p, nreg, e_reg, lanes, sh.kp);
   sh.kp.magic = 0x64646464u;
   sh.kp.one = 0x3C003C00u;
   // single-group register-message shapes address L absolutely: the table

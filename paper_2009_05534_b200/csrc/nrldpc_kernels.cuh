@@ -58,8 +58,13 @@ struct alignas(16) KParams {
   uint16_t row_start[NR_MAX_ROWS + 1];  // first edge of each row (message offsets)
   uint16_t tab_start[NR_MAX_ROWS + 1];  // row's first slot in sh/cb (multiple of 4)
   uint8_t bar_after[NR_MAX_ROWS];       // 0: next row is column-disjoint from this layer
-  // per row: x = tab_start | w << 16, y = first smem message slot | bar_after << 16
-  alignas(8) uint2 rowdesc[NR_MAX_ROWS + 2];
+  // layer units of the BG1/BG2 kernels after the register rows (one row or
+  // two fused column-disjoint rows): a = {code wa | wb << 8, barrier after,
+  // table byte offset of row a, message byte offset of row a}, b = the same
+  // offsets of row b. One spare entry for the one-ahead prefetch.
+  int n_units;
+  alignas(16) uint4 unit_a[NR_MAX_ROWS + 1];
+  alignas(8) uint2 unit_b[NR_MAX_ROWS + 1];
   // per-edge graph tables, each row padded to a multiple of 4 slots so a row
   // loads them with 128-bit uniform constant loads
   alignas(16) uint32_t sh[NR_MAX_TAB];  // shift * LANES (bytes)
