@@ -80,13 +80,13 @@ __device__ __forceinline__ uint32_t edge_offset(uint32_t shift, uint32_t colbase
   return a + colbase;
 }
 
-// A row's shift/column tables (tb = byte offset of its first slot, a
-// multiple of 16): 128-bit uniform loads.
+// A row's shift/column tables (tq = its first slot / 4; rows are padded to
+// 4 slots): 128-bit uniform loads.
 template <int MAXW>
-__device__ __forceinline__ void load_row_tables(const KParams& p, uint32_t tb, int w, uint32_t (&sh)[MAXW],
+__device__ __forceinline__ void load_row_tables(const KParams& p, uint32_t tq, int w, uint32_t (&sh)[MAXW],
                                                 uint32_t (&cb)[MAXW]) {
-  const uint4* S = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(p.sh) + tb);
-  const uint4* C = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(p.cb) + tb);
+  const uint4* S = reinterpret_cast<const uint4*>(p.sh) + tq;
+  const uint4* C = reinterpret_cast<const uint4*>(p.cb) + tq;
 #pragma unroll
   for (int k = 0; k < (MAXW + 3) / 4; ++k) {
     if (4 * k < w) {
@@ -192,7 +192,7 @@ struct RowWork {
   int w;
 
   // phase 1: gather L and the old messages, t = L - M, fold (m1, m2, S)
-  // tb: byte offset of the row's table slots; mb: byte offset of its first
+  // tb: the row's table slot / 4; mb: byte offset of its first
   // message in this thread's shared-memory message row
   __device__ __forceinline__ void gather(const KParams& p, const uint32_t tb, const uint32_t mb, const int w_,
                                          uint32_t zl, uint32_t ZL, const uint8_t* __restrict__ Lg,
@@ -487,7 +487,7 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
   if constexpr (BG == 0) {
     for (int r = 0; r < p.rows; ++r) {
       const int e0 = p.row_start[r];
-      process_row<MAXW, LANES, false>(p, 4u * p.tab_start[r], (uint32_t)e0 * LANES, p.row_start[r + 1] - e0, c.zl, c.ZL, c.Lg, c.Mz,
+      process_row<MAXW, LANES, false>(p, p.tab_start[r] / 4u, (uint32_t)e0 * LANES, p.row_start[r + 1] - e0, c.zl, c.ZL, c.Lg, c.Mz,
                                       rm.r4, c.lut, c.magic, c.one, c.st_ok);
       if (p.bar_after[r]) __syncthreads();
     }
@@ -496,19 +496,19 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
     if constexpr (NREG > 0) {
 #pragma unroll 1
       for (int r = 0; r < RegMsg<NREG>::nq; r += 2) {
-        process_row<19, LANES, true, ABS>(p, 80u * r, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, rm.q[0], c.lut, c.magic,
+        process_row<19, LANES, true, ABS>(p, 5u * r, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, rm.q[0], c.lut, c.magic,
                                      c.one, c.st_ok);
         __syncthreads();
-        process_row<19, LANES, true, ABS>(p, 80u * r + 80u, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, rm.q[1], c.lut,
+        process_row<19, LANES, true, ABS>(p, 5u * r + 5u, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, rm.q[1], c.lut,
                                      c.magic, c.one, c.st_ok);
         rm.rotate2();
         __syncthreads();
       }
       if constexpr (NREG == 6) {
-        process_row<3, LANES, true, ABS>(p, 320u, 0, 3, c.zl, c.ZL, c.Lg, c.Mz, rm.r4, c.lut, c.magic, c.one,
+        process_row<3, LANES, true, ABS>(p, 20u, 0, 3, c.zl, c.ZL, c.Lg, c.Mz, rm.r4, c.lut, c.magic, c.one,
                                     c.st_ok);
         __syncthreads();
-        process_row<8, LANES, true, ABS>(p, 336u, 0, 8, c.zl, c.ZL, c.Lg, c.Mz, rm.r5, c.lut, c.magic, c.one,
+        process_row<8, LANES, true, ABS>(p, 21u, 0, 8, c.zl, c.ZL, c.Lg, c.Mz, rm.r5, c.lut, c.magic, c.one,
                                     c.st_ok);
         __syncthreads();
       }
@@ -550,7 +550,7 @@ __device__ __forceinline__ void local_check(const KParams& p, uint32_t zl, uint3
   if constexpr (BG == 0) {
     for (int r = 0; r < p.rows; ++r) {
       const int e0 = p.row_start[r];
-      row_parity<MAXW, LANES>(p, 4u * p.tab_start[r], p.row_start[r + 1] - e0, zl, ZL, Lg, wa, wb);
+      row_parity<MAXW, LANES>(p, p.tab_start[r] / 4u, p.row_start[r + 1] - e0, zl, ZL, Lg, wa, wb);
     }
   } else {
 #pragma unroll 1
@@ -558,7 +558,7 @@ __device__ __forceinline__ void local_check(const KParams& p, uint32_t zl, uint3
       const int e0 = p.row_start[r];
       const int t0 = p.tab_start[r];
       dispatch_w<BG>(p.row_start[r + 1] - e0, [&](auto W) {
-        row_parity<decltype(W)::value, LANES, ABS>(p, 4u * t0, decltype(W)::value, zl, ZL, Lg, wa, wb);
+        row_parity<decltype(W)::value, LANES, ABS>(p, t0 / 4u, decltype(W)::value, zl, ZL, Lg, wa, wb);
       });
     }
   }
@@ -1095,12 +1095,12 @@ void build_units(const nrldpc_plan* p, int nreg, int e_reg, int lanes, KParams& 
   int n = 0;
   for (int r = nreg; r < p->rows;) {
     const int wa = b.row_start[r + 1] - b.row_start[r];
-    const uint32_t ta = 4u * b.tab_start[r], ma = (uint32_t)(b.row_start[r] - e_reg) * lanes;
+    const uint32_t ta = b.tab_start[r] / 4u, ma = (uint32_t)(b.row_start[r] - e_reg) * lanes;
     if (p->schedule != 0 && !b.bar_after[r] && r + 1 < p->rows) {
       const int wb = b.row_start[r + 2] - b.row_start[r + 1];
       if (fused_pair(p->schedule, wa, wb)) {
         kp.unit_a[n] = make_uint4((uint32_t)(wa | wb << 8), b.bar_after[r + 1], ta, ma);
-        kp.unit_b[n] = make_uint2(4u * b.tab_start[r + 1], (uint32_t)(b.row_start[r + 1] - e_reg) * lanes);
+        kp.unit_b[n] = make_uint2(b.tab_start[r + 1] / 4u, (uint32_t)(b.row_start[r + 1] - e_reg) * lanes);
         ++n;
         r += 2;
         continue;

@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
       const int e0 = p.row_start[r];
       const int w = p.row_start[r + 1] - e0;
       uint32_t tsh[19], tcb[19];
-      load_row_tables<19>(p, 4u * p.tab_start[r], w, tsh, tcb);
+      load_row_tables<19>(p, p.tab_start[r] / 4u, w, tsh, tcb);
       uint32_t off[19], t[19], neg[19];
       uint32_t m1 = F::sat(), m2 = F::sat(), S = 0;
 #pragma unroll
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
       for (int r = 0; r < p.rows; ++r) {
         const int w = p.row_start[r + 1] - p.row_start[r];
         uint32_t tsh[19], tcb[19];
-        load_row_tables<19>(p, 4u * p.tab_start[r], w, tsh, tcb);
+        load_row_tables<19>(p, p.tab_start[r] / 4u, w, tsh, tcb);
         uint32_t par = 0;
 #pragma unroll
         for (int j = 0; j < 19; ++j)

@@ -60,7 +60,7 @@ struct alignas(16) KParams {
   uint8_t bar_after[NR_MAX_ROWS];       // 0: next row is column-disjoint from this layer
   // layer units of the BG1/BG2 kernels after the register rows (one row or
   // two fused column-disjoint rows): a = {code wa | wb << 8, barrier after,
-  // table byte offset of row a, message byte offset of row a}, b = the same
+  // table slot / 4 of row a, message byte offset of row a}, b = the same
   // offsets of row b. One spare entry for the one-ahead prefetch.
   int n_units;
   alignas(16) uint4 unit_a[NR_MAX_ROWS + 1];
