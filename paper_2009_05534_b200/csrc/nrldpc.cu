@@ -108,8 +108,8 @@ __device__ __forceinline__ void load_row_tables(const KParams& p, uint32_t tq, i
 // Registers (REGMSG, LANES=2): two 16-bit message pairs per 32-bit register,
 // edge e in half (e & 1) of mreg[e >> 1]; e is a compile-time constant after
 // the schedule is unrolled, so mreg stays in registers.
-template <int LANES, bool REGMSG>
-__device__ __forceinline__ half2 msg_load(const uint8_t* Mrow, const uint32_t* mreg, int j, int e,
+template <int LANES, bool REGMSG, bool ABS = false>
+__device__ __forceinline__ half2 msg_load(const uint8_t* Mrow, uint32_t Ms, const uint32_t* mreg, int j, int e,
                                           uint32_t magic) {
   if constexpr (REGMSG) {
     uint32_t d;
@@ -117,17 +117,19 @@ __device__ __forceinline__ half2 msg_load(const uint8_t* Mrow, const uint32_t* m
     else asm("prmt.b32 %0, %1, %2, 0x4140;" : "=r"(d) : "r"(mreg[e >> 1]), "r"(magic));
     return u2h(d);
   } else {
-    return unpack_elem<LANES>(ld_elem<LANES>(Mrow + j * LANES), magic);
+    const uint32_t raw = ABS ? lds_elem<LANES>(Ms + j * LANES) : ld_elem<LANES>(Mrow + j * LANES);
+    return unpack_elem<LANES>(raw, magic);
   }
 }
 
-template <int LANES, bool REGMSG>
-__device__ __forceinline__ void msg_store(uint8_t* Mrow, uint32_t* mreg, int j, int e, half2 biased,
+template <int LANES, bool REGMSG, bool ABS = false>
+__device__ __forceinline__ void msg_store(uint8_t* Mrow, uint32_t Ms, uint32_t* mreg, int j, int e, half2 biased,
                                           bool st_ok) {
   if constexpr (REGMSG) {
     mreg[e >> 1] = __byte_perm(h2u(biased), mreg[e >> 1], (e & 1) ? 0x2054 : 0x7620);
   } else {
-    st_elem_if<LANES>(Mrow + j * LANES, pack_elem<LANES>(biased), st_ok);
+    if constexpr (ABS) sts_elem_if<LANES>(Ms + j * LANES, pack_elem<LANES>(biased), st_ok);
+    else st_elem_if<LANES>(Mrow + j * LANES, pack_elem<LANES>(biased), st_ok);
   }
 }
 
@@ -189,6 +191,7 @@ struct RowWork {
   half2 m1, m2;
   uint32_t S;
   uint8_t* Mrow;
+  uint32_t Ms;  // ABS: shared-window address of Mrow
   int w;
 
   // phase 1: gather L and the old messages, t = L - M, fold (m1, m2, S)
@@ -196,10 +199,12 @@ struct RowWork {
   // message in this thread's shared-memory message row
   __device__ __forceinline__ void gather(const KParams& p, const uint32_t tb, const uint32_t mb, const int w_,
                                          uint32_t zl, uint32_t ZL, const uint8_t* __restrict__ Lg,
-                                         uint8_t* __restrict__ Mz, const uint32_t* mreg, uint32_t magic) {
+                                         uint8_t* __restrict__ Mz, uint32_t Mzs, const uint32_t* mreg,
+                                         uint32_t magic) {
     const half2 H127 = u2h(0x57F057F0u);
     w = w_;
     Mrow = Mz + mb;
+    Ms = Mzs + mb;
     uint32_t tsh[MAXW], tcb[MAXW];
     load_row_tables<MAXW>(p, tb, w, tsh, tcb);
     m1 = H127;
@@ -211,7 +216,7 @@ struct RowWork {
         off[j] = edge_offset(tsh[j], tcb[j], zl, ZL);
         const uint32_t raw = ABS ? lds_elem<LANES>(off[j]) : ld_elem<LANES>(Lg + off[j]);
         const half2 lh = unpack_elem<LANES>(raw, magic);
-        const half2 mh = msg_load<LANES, REGMSG>(Mrow, mreg, j, j, magic);
+        const half2 mh = msg_load<LANES, REGMSG, ABS>(Mrow, Ms, mreg, j, j, magic);
         const half2 tj = __hsub2(lh, mh);           // exact: L - M
         S ^= h2u(tj);                               // sign product (bits 15/31)
         t[j] = tj;
@@ -275,7 +280,7 @@ struct RowWork {
         const uint32_t lnew = pack_elem<LANES>(__hfma2(y, sg, H1152));
         if constexpr (ABS) sts_elem_if<LANES>(off[j], lnew, st_ok);
         else st_elem_if<LANES>(Lg + off[j], lnew, st_ok);
-        msg_store<LANES, REGMSG>(Mrow, mreg, j, j, __hfma2(mag, sg, H1152), st_ok);
+        msg_store<LANES, REGMSG, ABS>(Mrow, Ms, mreg, j, j, __hfma2(mag, sg, H1152), st_ok);
       }
     }
   }
@@ -284,11 +289,11 @@ struct RowWork {
 template <int MAXW, int LANES, bool REGMSG, bool ABS = false>
 __device__ __forceinline__ void process_row(const KParams& p, const uint32_t tb, const uint32_t mb, const int w,
                                             uint32_t zl, uint32_t ZL, uint8_t* __restrict__ Lg,
-                                            uint8_t* __restrict__ Mz, uint32_t* mreg,
+                                            uint8_t* __restrict__ Mz, uint32_t Mzs, uint32_t* mreg,
                                             const uint16_t* __restrict__ lut, uint32_t magic,
                                             uint32_t one, bool st_ok) {
   RowWork<MAXW, LANES, REGMSG, ABS> r;
-  r.gather(p, tb, mb, w, zl, ZL, Lg, Mz, mreg, magic);
+  r.gather(p, tb, mb, w, zl, ZL, Lg, Mz, Mzs, mreg, magic);
   if (p.beta_mode) r.beta_arith(p, one);
   else r.beta_lut(lut, one);
   r.scatter(Lg, mreg, one, st_ok);
@@ -300,13 +305,13 @@ template <int WA, int WB, int LANES, bool ABS = false>
 __device__ __forceinline__ void process_rows2(const KParams& p, uint32_t tba, uint32_t mba, uint32_t tbb,
                                               uint32_t mbb,
                                               uint32_t zl, uint32_t ZL, uint8_t* __restrict__ Lg,
-                                              uint8_t* __restrict__ Mz, uint32_t* mreg,
+                                              uint8_t* __restrict__ Mz, uint32_t Mzs, uint32_t* mreg,
                                               const uint16_t* __restrict__ lut, uint32_t magic,
                                               uint32_t one, bool st_ok) {
   RowWork<WA, LANES, false, ABS> a;
   RowWork<WB, LANES, false, ABS> b;
-  a.gather(p, tba, mba, WA, zl, ZL, Lg, Mz, mreg, magic);
-  b.gather(p, tbb, mbb, WB, zl, ZL, Lg, Mz, mreg, magic);
+  a.gather(p, tba, mba, WA, zl, ZL, Lg, Mz, Mzs, mreg, magic);
+  b.gather(p, tbb, mbb, WB, zl, ZL, Lg, Mz, Mzs, mreg, magic);
   if (p.beta_mode) {
     a.beta_arith(p, one);
     b.beta_arith(p, one);
@@ -365,6 +370,7 @@ struct RowCtx {
   uint32_t zl, ZL;
   uint8_t* Lg;
   uint8_t* Mz;
+  uint32_t Ms;  // shared-window address of Mz
   const uint16_t* lut;
   uint32_t magic, one;
   bool st_ok;
@@ -487,7 +493,7 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
   if constexpr (BG == 0) {
     for (int r = 0; r < p.rows; ++r) {
       const int e0 = p.row_start[r];
-      process_row<MAXW, LANES, false>(p, p.tab_start[r] / 4u, (uint32_t)e0 * LANES, p.row_start[r + 1] - e0, c.zl, c.ZL, c.Lg, c.Mz,
+      process_row<MAXW, LANES, false>(p, p.tab_start[r] / 4u, (uint32_t)e0 * LANES, p.row_start[r + 1] - e0, c.zl, c.ZL, c.Lg, c.Mz, c.Ms,
                                       rm.r4, c.lut, c.magic, c.one, c.st_ok);
       if (p.bar_after[r]) __syncthreads();
     }
@@ -496,19 +502,19 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
     if constexpr (NREG > 0) {
 #pragma unroll 1
       for (int r = 0; r < RegMsg<NREG>::nq; r += 2) {
-        process_row<19, LANES, true, ABS>(p, 5u * r, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, rm.q[0], c.lut, c.magic,
+        process_row<19, LANES, true, ABS>(p, 5u * r, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.q[0], c.lut, c.magic,
                                      c.one, c.st_ok);
         __syncthreads();
-        process_row<19, LANES, true, ABS>(p, 5u * r + 5u, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, rm.q[1], c.lut,
+        process_row<19, LANES, true, ABS>(p, 5u * r + 5u, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.q[1], c.lut,
                                      c.magic, c.one, c.st_ok);
         rm.rotate2();
         __syncthreads();
       }
       if constexpr (NREG == 6) {
-        process_row<3, LANES, true, ABS>(p, 20u, 0, 3, c.zl, c.ZL, c.Lg, c.Mz, rm.r4, c.lut, c.magic, c.one,
+        process_row<3, LANES, true, ABS>(p, 20u, 0, 3, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r4, c.lut, c.magic, c.one,
                                     c.st_ok);
         __syncthreads();
-        process_row<8, LANES, true, ABS>(p, 21u, 0, 8, c.zl, c.ZL, c.Lg, c.Mz, rm.r5, c.lut, c.magic, c.one,
+        process_row<8, LANES, true, ABS>(p, 21u, 0, 8, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r5, c.lut, c.magic, c.one,
                                     c.st_ok);
         __syncthreads();
       }
@@ -530,10 +536,10 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
       dispatch_unit<BG>(A.x, [&](auto WA, auto WB) {
         constexpr int wa = decltype(WA)::value, wb = decltype(WB)::value;
         if constexpr (wb == 0)
-          process_row<wa, LANES, false, ABS>(p, A.z, A.w, wa, c.zl, c.ZL, c.Lg, c.Mz, rm.r4, c.lut, c.magic,
+          process_row<wa, LANES, false, ABS>(p, A.z, A.w, wa, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r4, c.lut, c.magic,
                                              c.one, c.st_ok);
         else
-          process_rows2<wa, wb, LANES, ABS>(p, A.z, A.w, B.x, B.y, c.zl, c.ZL, c.Lg, c.Mz, rm.r4, c.lut,
+          process_rows2<wa, wb, LANES, ABS>(p, A.z, A.w, B.x, B.y, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r4, c.lut,
                                             c.magic, c.one, c.st_ok);
       });
       // consecutive column-disjoint rows form one layer: the next unit reads
@@ -723,7 +729,7 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
 
   const uint32_t magic = p.magic;  // 0x64646464, opaque to ptxas
   const uint32_t one = p.one;      // 0x3C003C00 (half2 1.0)
-  const RowCtx rc{zl, ZL, Lg, Mz, lut, magic, one, st_ok};
+  const RowCtx rc{zl, ZL, Lg, Mz, (uint32_t)__cvta_generic_to_shared(Mz), lut, magic, one, st_ok};
   RegMsg<NREG> rm;
   rm.init();
   for (int it = 1; it <= p.max_iter; ++it) {
