@@ -69,6 +69,15 @@ int nrldpc_plan_create(int device, int k_b, int z, int rows_used,
 
 int nrldpc_plan_destroy(nrldpc_plan* plan);
 
+/*
+ * Scheduling hint (no reference counterpart; results are unchanged): the
+ * plan's launches will run concurrently with other plans' launches on the
+ * same SMs, as in a mixed-shape batch. Selects the
+ * int8 kernel variant measured fastest under co-scheduling. Call before the
+ * plan's first decode; not safe concurrently with decodes on the same plan.
+ */
+int nrldpc_plan_set_coscheduled(nrldpc_plan* plan, int on);
+
 /* K = k_b*z info bits, n_c = z*(k_b+rows_used), words = ceil(K/32). */
 int nrldpc_plan_info(const nrldpc_plan* plan, int64_t* k, int64_t* n_c,
                      int64_t* n_tx, int64_t* words_per_cw, int* lanes,

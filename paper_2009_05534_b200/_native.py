@@ -27,6 +27,7 @@ IN_F64, IN_F32 = 0, 1
 EXPORTS = (
     "nrldpc_plan_create",
     "nrldpc_plan_destroy",
+    "nrldpc_plan_set_coscheduled",
     "nrldpc_plan_info",
     "nrldpc_quantize",
     "nrldpc_demap_quantize",
@@ -69,6 +70,8 @@ def load() -> ctypes.CDLL:
     lib.nrldpc_plan_create.restype = c_int
     lib.nrldpc_plan_destroy.argtypes = [c_void_p]
     lib.nrldpc_plan_destroy.restype = c_int
+    lib.nrldpc_plan_set_coscheduled.argtypes = [c_void_p, c_int]
+    lib.nrldpc_plan_set_coscheduled.restype = c_int
     lib.nrldpc_plan_info.argtypes = [c_void_p] + [c_void_p] * 8
     lib.nrldpc_plan_info.restype = c_int
     lib.nrldpc_quantize.argtypes = [c_void_p, c_void_p, c_int, c_int64, c_double, c_double, c_void_p,

@@ -911,6 +911,7 @@ struct Shape {
 
 struct nrldpc_plan {
   int device = 0;
+  bool coscheduled = false;  // launches share SMs with other plans' launches
   int precision = NRLDPC_INT8;
   int early_stop = NRLDPC_STOP_SYNDROME;
   int crc_kind = NRLDPC_CRC24B;
@@ -1130,17 +1131,24 @@ Shape choose_shape(const nrldpc_plan* p, int max_lanes) {
   };
   int lanes = 1, nreg = 0;
   if (max_lanes >= 2) {
-    if (smem_for(1, align16(n_pos * 2), msg_bytes(2, 0)) <= smem_max) {
+    const bool fits = smem_for(1, align16(n_pos * 2), msg_bytes(2, 0)) <= smem_max;
+    // BG1 pairs with Z > 256 run one group per CTA; they keep the messages
+    // of rows 0..5 in registers whenever those rows exist (fewer shared
+    // accesses, and one kernel for all large Z, which matters when many Z
+    // decode concurrently). Rows 0..1 / 0..3 when rows_used < 6.
+    const bool big = p->schedule == 1 && p->z > 256 && p->z <= 384;
+    if (fits && !big) {
       lanes = 2;
-    } else if (p->schedule == 1) {
-      for (int nr : {2, 4, 6}) {
-        if (nr > p->rows || p->z > 384) break;
+    } else if (p->schedule == 1 && p->z <= 384) {
+      for (int nr : {6, 4, 2}) {
+        if (nr > p->rows) continue;
         if (smem_for(1, align16(n_pos * 2), msg_bytes(2, RowW<1>::e0[nr])) <= smem_max) {
           lanes = 2;
           nreg = nr;
           break;
         }
       }
+      if (!nreg && fits) lanes = 2;
     }
   }
   const int e_reg = nreg ? RowW<1>::e0[nreg] : 0;
@@ -1177,10 +1185,15 @@ Shape choose_shape(const nrldpc_plan* p, int max_lanes) {
   build_units(p, nreg, e_reg, lanes, sh.kp);
   sh.kp.magic = 0x64646464u;
   sh.kp.one = 0x3C003C00u;
-  // single-group register-message shapes address L absolutely: the table
-  // holds column base + the L array's shared-window address (the dynamic
-  // window starts after the 1 KB system reservation; the kernel verifies)
-  sh.kp.abs_base = (nreg > 0 && best_g == 1) ? kSmemWindowBase + data_offset(1) : 0u;
+  // single-group pair shapes of the BG1/BG2 schedules address L absolutely:
+  // the table holds column base + the L array's shared-window address (the
+  // dynamic window starts after the 1 KB system reservation; the kernel
+  // verifies)
+  // Absolute L addressing is ~5% faster for one decode alone, but measured
+  // ~12% slower when many plans' kernels share the SMs (mixed-shape batches,
+  // nrldpc_plan_set_coscheduled); register-row shapes always use it.
+  const bool abs = best_g == 1 && lanes == 2 && p->schedule != 0 && (nreg > 0 || !p->coscheduled);
+  sh.kp.abs_base = abs ? kSmemWindowBase + data_offset(1) : 0u;
   sh.abs = sh.kp.abs_base != 0;
   for (int t = 0; t < NR_MAX_TAB; ++t) {
     sh.kp.sh[t] = p->base.sh[t] * lanes;
@@ -1198,13 +1211,17 @@ static cudaError_t launch_shape(const nrldpc_plan* plan, Shape& sh, const int8_t
   switch (plan->schedule) {
     case 1:
       if (!two) return launch_i8<1, 19, 1>(sh, dev, in, batch, o, st);
-      if (sh.nreg == 0) return launch_i8<1, 19, 2>(sh, dev, in, batch, o, st);
+      if (sh.nreg == 0)
+        return sh.abs ? launch_i8<1, 19, 2, 0, true>(sh, dev, in, batch, o, st)
+                      : launch_i8<1, 19, 2>(sh, dev, in, batch, o, st);
       if (!sh.abs) return cudaErrorInvalidConfiguration;
       if (sh.nreg == 2) return launch_i8<1, 19, 2, 2, true>(sh, dev, in, batch, o, st);
       if (sh.nreg == 4) return launch_i8<1, 19, 2, 4, true>(sh, dev, in, batch, o, st);
       return launch_i8<1, 19, 2, 6, true>(sh, dev, in, batch, o, st);
     case 2:
-      return two ? launch_i8<2, 10, 2>(sh, dev, in, batch, o, st) : launch_i8<2, 10, 1>(sh, dev, in, batch, o, st);
+      if (!two) return launch_i8<2, 10, 1>(sh, dev, in, batch, o, st);
+      return sh.abs ? launch_i8<2, 10, 2, 0, true>(sh, dev, in, batch, o, st)
+                    : launch_i8<2, 10, 2>(sh, dev, in, batch, o, st);
     default:
       if (plan->maxw > 10)
         return two ? launch_i8<0, 19, 2>(sh, dev, in, batch, o, st) : launch_i8<0, 19, 1>(sh, dev, in, batch, o, st);
@@ -1630,6 +1647,23 @@ int nrldpc_plan_create(int device, int k_b, int z, int rows_used, const int32_t*
     }
   }
   *out = p;
+  return NRLDPC_OK;
+}
+
+int nrldpc_plan_set_coscheduled(nrldpc_plan* plan, int on) {
+  if (!plan) return fail(NRLDPC_EINVAL, "plan is NULL");
+  if (plan->precision != NRLDPC_INT8 || plan->coscheduled == (on != 0)) return NRLDPC_OK;
+  plan->coscheduled = on != 0;
+  const char* force = std::getenv("NRLDPC_FORCE_LANES");
+  Shape sh = choose_shape(plan, force && force[0] == '1' ? 1 : 2);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(plan->device);
+  KOut none{};
+  const cudaError_t e = launch_shape(plan, sh, nullptr, 0, none, nullptr);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return cuda_fail(e, "kernel setup");
+  plan->main = sh;
   return NRLDPC_OK;
 }
 

@@ -111,7 +111,7 @@ _STOP_CODE = {EarlyStop.SYNDROME: _native.STOP_SYNDROME, EarlyStop.CRC: _native.
 class Plan:
     """Owns one ``nrldpc_plan`` (graph tables + config baked for one device)."""
 
-    def __init__(self, bg, rows_used: int, cfg: DecodeConfig, device: int = 0):
+    def __init__(self, bg, rows_used: int, cfg: DecodeConfig, device: int = 0, coscheduled: bool = False):
         lib = _native.load()
         self.tables = edge_tables(bg, rows_used)
         self.cfg = cfg
@@ -126,6 +126,10 @@ class Plan:
             _PREC_CODE[cfg.precision], float(cfg.beta), int(cfg.max_iter),
             _STOP_CODE[cfg.early_stop], _native.CRC_KINDS[cfg.crc_kind], ctypes.byref(handle)))
         self.handle = handle
+        self.coscheduled = bool(coscheduled)
+        if coscheduled:
+            # launches share SMs with other plans' (mixed-shape batches)
+            _native.check(lib.nrldpc_plan_set_coscheduled(handle, 1))
         vals = [ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(),
                 ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int64()]
         _native.check(lib.nrldpc_plan_info(handle, *[ctypes.byref(v) for v in vals]))
@@ -223,13 +227,14 @@ _PLAN_CACHE: dict = {}
 _PLAN_LOCK = threading.Lock()
 
 
-def get_plan(bg, rows_used: int, cfg: DecodeConfig, device: int = 0) -> Plan:
+def get_plan(bg, rows_used: int, cfg: DecodeConfig, device: int = 0, coscheduled: bool = False) -> Plan:
     key = (str(bg.id).upper(), int(bg.z), int(rows_used), _graph_fingerprint(bg, rows_used),
-           cfg.precision, float(cfg.beta), int(cfg.max_iter), cfg.early_stop, cfg.crc_kind, device)
+           cfg.precision, float(cfg.beta), int(cfg.max_iter), cfg.early_stop, cfg.crc_kind, device,
+           bool(coscheduled))
     with _PLAN_LOCK:
         plan = _PLAN_CACHE.get(key)
         if plan is None:
-            plan = Plan(bg, rows_used, cfg, device)
+            plan = Plan(bg, rows_used, cfg, device, coscheduled)
             _PLAN_CACHE[key] = plan
         return plan
 

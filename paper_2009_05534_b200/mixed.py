@@ -32,7 +32,8 @@ class MixedBatchDecoder:
 
         self.cfg = cfg
         self.groups = groups
-        self.plans = [get_plan(g.bg, g.rows_used, cfg, device) for g in groups]
+        # plans tuned for sharing SMs with each other's launches
+        self.plans = [get_plan(g.bg, g.rows_used, cfg, device, coscheduled=True) for g in groups]
         dev = torch.device("cuda", device)
         dtype = {"int8": torch.int8, "f16": torch.float16, "f32": torch.float32}[cfg.precision.value]
         # static buffers: callers fill .inputs[i] (or pass arrays to decode())
@@ -40,17 +41,40 @@ class MixedBatchDecoder:
                        for g, p in zip(groups, self.plans)]
         self.outputs = [p.alloc_outputs(g.batch) for g, p in zip(groups, self.plans)]
         self._streams = [torch.cuda.Stream(device=dev) for _ in range(max(1, streams))]
+        self._order = self._schedule(len(self._streams))
         self._graph = None
         self._device = dev
+
+    def _schedule(self, n_streams: int) -> list[tuple[int, int]]:
+        """Longest-first list scheduling of the groups onto the side streams.
+
+        A group's kernel runs ceil(batch / codewords_per_cta) CTAs whose
+        duration grows with the edges each thread walks per iteration and
+        the CTA's warp count. The longest groups are launched first and each
+        goes to the stream with the least queued work, so the longest
+        kernels are not stuck behind short ones in launch order."""
+        sms = 148
+        costs = []
+        for g, p in zip(self.groups, self.plans):
+            ctas = -(-g.batch // max(1, p.codewords_per_cta))
+            warps = -(-p.threads_per_cta // 32)
+            per_cta = p.tables.n_edges * (1.0 + 0.05 * warps)
+            costs.append(per_cta * -(-ctas // sms))
+        queued = [0.0] * n_streams
+        order = []
+        for i in sorted(range(len(costs)), key=lambda i: -costs[i]):
+            s = min(range(n_streams), key=lambda k: queued[k])
+            queued[s] += costs[i]
+            order.append((i, s))
+        return order
 
     def _launch_all(self):
         import torch
         cur = torch.cuda.current_stream(self._device)
         for s in self._streams:
             s.wait_stream(cur)
-        for i, (plan, x, out) in enumerate(zip(self.plans, self.inputs, self.outputs)):
-            s = self._streams[i % len(self._streams)]
-            plan.decode_device(x, out, stream=s.cuda_stream)
+        for i, si in self._order:
+            self.plans[i].decode_device(self.inputs[i], self.outputs[i], stream=self._streams[si].cuda_stream)
         for s in self._streams:
             cur.wait_stream(s)
 

@@ -276,6 +276,25 @@ def test_mixed_batch_cuda_graph_matches_per_group(cuda_ok):
             assert_same(res, ref["bits"], ref["iterations"], ref["success"], ref["syndrome_weight"])
 
 
+@pytest.mark.parametrize("bg_id,z,rows", [("BG1", 256, 46), ("BG2", 384, 42), ("BG1", 320, 10),
+                                          ("BG2", 96, 7)])
+def test_coscheduled_plan_variant_is_bit_exact(cuda_ok, bg_id, z, rows):
+    """The co-scheduling hint only swaps the kernel variant: same results."""
+    bg = nr.load_basegraph(bg_id, z)
+    cfg = nr.DecodeConfig(max_iter=6, early_stop="syndrome")
+    _, llr = noisy_llrs(bg, rows, 1.5, 9, seed=(z, rows, 11))
+    blocks = oracle.quantize_i8(llr, z)
+    ref = oracle.decode(blocks, bg, cfg)
+    for co in (False, True):
+        plan = nr.Plan(bg, rows, cfg, coscheduled=co)
+        x = torch.from_numpy(blocks).cuda()
+        out = plan.alloc_outputs(len(blocks))
+        plan.decode_device(x, out)
+        bits = nr.unpack_bits(out["bits"].cpu().numpy(), plan.k)
+        assert np.array_equal(bits, ref["bits"]), co
+        assert np.array_equal(out["iters"].cpu().numpy(), ref["iterations"]), co
+
+
 @pytest.mark.parametrize("bg_id,z,rows", [("BG1", 384, 46), ("BG2", 13, 42), ("BG1", 7, 9),
                                           ("BG2", 240, 4), ("BG1", 2, 46)])
 def test_gpu_encoder_matches_host_encoder(cuda_ok, bg_id, z, rows):
