@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--chunks", type=int, default=4, help="e2e pipelining sub-batches")
+    ap.add_argument("--overlap", type=int, default=2,
+                    help="streams that consecutive (independent) batches alternate over; the tail "
+                         "wave of one batch's decode overlaps the next batch's first wave")
     return ap.parse_args()
 
 
@@ -220,8 +223,10 @@ def run_ours(args):
     per = blocks0.numel()
     nbuf = max(2, int(np.ceil(2.0 * 126e6 / per)) + 1)
     bufs = [torch.roll(blocks0, shifts=i, dims=0).contiguous() for i in range(nbuf)]
-    outs = [plan.alloc_outputs(B) for _ in range(2)]
+    n_ov = max(1, args.overlap)
+    outs = [plan.alloc_outputs(B) for _ in range(max(2, n_ov))]
     stream = torch.cuda.current_stream(dev)
+    side = [torch.cuda.Stream(device=dev) for _ in range(n_ov)]
 
     for i in range(args.warmup):
         plan.decode_device(bufs[i % nbuf], outs[i % 2])
@@ -233,9 +238,35 @@ def run_ours(args):
     bits = nr.unpack_bits(outs[0]["bits"].cpu().numpy(), k)
     bler = float((bits != msgs).any(axis=1).mean())
     success = float(outs[0]["success"].float().mean().item())
+    # the same inputs with the reference's syndrome early stop (quality check;
+    # fixed-iteration int8 decoding overshoots in the reference itself)
+    cfg_s = nr.DecodeConfig(max_iter=args.iters, early_stop="syndrome")
+    plan_s = nr.get_plan(bg, rows, cfg_s, device=local)
+    out_s = plan_s.alloc_outputs(B)
+    plan_s.decode_device(bufs[0], out_s)
+    torch.cuda.synchronize(dev)
+    bits_s = nr.unpack_bits(out_s["bits"].cpu().numpy(), k)
+    quality = {"bler_syndrome_stop": float((bits_s != msgs).any(axis=1).mean()),
+               "mean_iterations_syndrome_stop": float(out_s["iters"].float().mean().item()),
+               "note": "bler/success_rate are for the benchmarked fixed-iteration mode and match the "
+                       "reference bit for bit: its int8 engine with early_stop='none' diverges once "
+                       "converged (noise-free codewords fail from iteration 2; golden case "
+                       "cfg2_bg1_z384_none10 records success=0 for the reference itself)"}
 
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    # (1) batch latency and per-launch kernel time: one stream, back to back
+    n_lat = min(args.steps, 100)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(n_lat)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(n_lat)]
+    torch.cuda.synchronize(dev)
+    for i in range(n_lat):
+        starts[i].record(stream)
+        plan.decode_device(bufs[i % nbuf], outs[i % 2])
+        ends[i].record(stream)
+    torch.cuda.synchronize(dev)
+    step_ms = np.array([s.elapsed_time(e) for s, e in zip(starts, ends)])
+
+    # (2) throughput: K consecutive independent batches, alternating over
+    # n_ov streams, bracketed by events on the launching stream
     t_all0 = torch.cuda.Event(enable_timing=True)
     t_all1 = torch.cuda.Event(enable_timing=True)
     if world > 1:
@@ -244,14 +275,16 @@ def run_ours(args):
     sampler = ClockSampler(local)
     with sampler:
         t_all0.record(stream)
+        for s in side:
+            s.wait_stream(stream)
         for i in range(args.steps):
-            starts[i].record(stream)
-            plan.decode_device(bufs[i % nbuf], outs[i % 2])
-            ends[i].record(stream)
+            j = i % n_ov
+            plan.decode_device(bufs[i % nbuf], outs[j], stream=side[j].cuda_stream)
+        for s in side:
+            stream.wait_stream(s)
         t_all1.record(stream)
         torch.cuda.synchronize(dev)
     launches = args.steps  # one decode kernel per step
-    step_ms = np.array([s.elapsed_time(e) for s, e in zip(starts, ends)])
     total_ms = t_all0.elapsed_time(t_all1)
     if world > 1:
         t = torch.tensor([total_ms], device=dev)
@@ -288,10 +321,12 @@ def run_ours(args):
                    "codewords_per_cta": plan.codewords_per_cta, "threads_per_cta": plan.threads_per_cta,
                    "smem_bytes": plan.smem_bytes,
                    "l2": f"inputs rotate over {nbuf} buffers ({nbuf * per / 1e6:.0f} MB > 126 MB L2)",
-                   "parallelism": f"batch shard x{world}, no collective"},
+                   "parallelism": f"batch shard x{world}, no collective",
+                   "overlap": f"{n_ov} streams: consecutive independent batches alternate, so one "
+                              f"batch's partial last wave shares the SMs with the next batch's first"},
         "p50_batch_latency_ms": float(np.median(step_ms)),
         "p99_batch_latency_ms": float(np.percentile(step_ms, 99)),
-        "bler": bler, "success_rate": success,
+        "bler": bler, "success_rate": success, "quality": quality,
         "roofline": {
             "bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s",
             "frac": achieved / peak_ops, "traffic": None,
