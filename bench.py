@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
-    ap.add_argument("--chunks", type=int, default=4, help="e2e pipelining sub-batches")
+    ap.add_argument("--chunks", type=int, default=12, help="e2e pipelining sub-batches")
     ap.add_argument("--overlap", type=int, default=2,
                     help="streams that consecutive (independent) batches alternate over; the tail "
                          "wave of one batch's decode overlaps the next batch's first wave")

@@ -927,7 +927,11 @@ struct nrldpc_plan {
   Shape main;        // the launch shape
   // host-path staging (nrldpc_decode_host)
   std::mutex host_mu;
-  cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
+  // host pipeline: streams[0] copies in (in chunk order) and out; the rest
+  // decode chunks as their input lands (one event per chunk)
+  static constexpr int kHostStreams = 17;
+  cudaStream_t streams[kHostStreams] = {};
+  std::vector<cudaEvent_t> chunk_ev;
   void* d_buf = nullptr;
   size_t d_cap = 0;
 };
@@ -1674,6 +1678,7 @@ int nrldpc_plan_destroy(nrldpc_plan* plan) {
   cudaSetDevice(plan->device);
   for (auto& s : plan->streams)
     if (s) cudaStreamDestroy(s);
+  for (auto& e : plan->chunk_ev) cudaEventDestroy(e);
   if (plan->d_buf) cudaFree(plan->d_buf);
   if (plan->d_crc_tab) cudaFree(plan->d_crc_tab);
   cudaSetDevice(prev);
@@ -1816,34 +1821,66 @@ int nrldpc_decode_host(nrldpc_plan* plan, const void* llr_host, int64_t batch, u
   uint8_t* d_succ = reinterpret_cast<uint8_t*>(d_synd) + align16(batch * 4);
   uint8_t* d_crc = d_succ + align16(batch);
   int32_t* d_status = reinterpret_cast<int32_t*>(d_crc + align16(batch));
-  NR_CUDA(cudaMemsetAsync(d_status, 0, 4, plan->streams[0]));
-  NR_CUDA(cudaStreamSynchronize(plan->streams[0]));
+  // Pipeline: the copy stream moves the chunks in order at full link rate,
+  // each chunk's decode waits only for its own input, and many chunk kernels
+  // are in flight at once so their partial waves pack the SMs. Results come
+  // back in one pass at the end (they are ~4% of the input bytes).
+  cudaStream_t cp = plan->streams[0];
+  constexpr int n_comp = nrldpc_plan::kHostStreams - 1;
+  static const bool dbg = getenv("NRLDPC_HOST_TIMING") != nullptr;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  if (dbg) {
+    cudaEventCreate(&t0);
+    cudaEventCreate(&t1);
+    cudaEventRecord(t0, cp);
+  }
+  NR_CUDA(cudaMemsetAsync(d_status, 0, 4, cp));
   if (chunks < 1) chunks = 1;
   const int64_t per_lane_cta = (int64_t)plan->main.groups * plan->main.lanes;
   int64_t chunk = (batch + chunks - 1) / chunks;
   chunk = (chunk + per_lane_cta - 1) / per_lane_cta * per_lane_cta;
+  const int n_chunks = (int)((batch + chunk - 1) / chunk);
+  while ((int)plan->chunk_ev.size() < n_chunks + n_comp) {
+    cudaEvent_t e;
+    NR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    plan->chunk_ev.push_back(e);
+  }
   int launches = 0;
-  int idx = 0;
-  for (int64_t b0 = 0; b0 < batch; b0 += chunk, ++idx) {
+  for (int idx = 0; idx < n_chunks; ++idx) {
+    const int64_t b0 = idx * chunk;
     const int64_t nb = std::min<int64_t>(chunk, batch - b0);
-    cudaStream_t st = plan->streams[idx % 3];
     NR_CUDA(cudaMemcpyAsync(d_llr + b0 * per_cw_in, static_cast<const uint8_t*>(llr_host) + b0 * per_cw_in,
-                            nb * per_cw_in, cudaMemcpyHostToDevice, st));
+                            nb * per_cw_in, cudaMemcpyHostToDevice, cp));
+    NR_CUDA(cudaEventRecord(plan->chunk_ev[idx], cp));
+    cudaStream_t st = plan->streams[1 + idx % n_comp];
+    NR_CUDA(cudaStreamWaitEvent(st, plan->chunk_ev[idx], 0));
     KOut o{d_bits + b0 * words, d_iters + b0, d_synd + b0, d_succ + b0,
            crc_ok ? d_crc + b0 : nullptr, nullptr, nullptr, d_status};
     g_launches = 0;
     const int rc = decode_impl(plan, d_llr + b0 * per_cw_in, nb, o, st);
     if (rc != NRLDPC_OK) return rc;
     launches += g_launches;
-    NR_CUDA(cudaMemcpyAsync(bits + b0 * words, d_bits + b0 * words, nb * words * 4, cudaMemcpyDeviceToHost, st));
-    NR_CUDA(cudaMemcpyAsync(iters + b0, d_iters + b0, nb * 4, cudaMemcpyDeviceToHost, st));
-    NR_CUDA(cudaMemcpyAsync(synd + b0, d_synd + b0, nb * 4, cudaMemcpyDeviceToHost, st));
-    NR_CUDA(cudaMemcpyAsync(success + b0, d_succ + b0, nb, cudaMemcpyDeviceToHost, st));
-    if (crc_ok) NR_CUDA(cudaMemcpyAsync(crc_ok + b0, d_crc + b0, nb, cudaMemcpyDeviceToHost, st));
   }
+  for (int c = 0; c < n_comp; ++c) {
+    NR_CUDA(cudaEventRecord(plan->chunk_ev[n_chunks + c], plan->streams[1 + c]));
+    NR_CUDA(cudaStreamWaitEvent(cp, plan->chunk_ev[n_chunks + c], 0));
+  }
+  NR_CUDA(cudaMemcpyAsync(bits, d_bits, batch * words * 4, cudaMemcpyDeviceToHost, cp));
+  NR_CUDA(cudaMemcpyAsync(iters, d_iters, batch * 4, cudaMemcpyDeviceToHost, cp));
+  NR_CUDA(cudaMemcpyAsync(synd, d_synd, batch * 4, cudaMemcpyDeviceToHost, cp));
+  NR_CUDA(cudaMemcpyAsync(success, d_succ, batch, cudaMemcpyDeviceToHost, cp));
+  if (crc_ok) NR_CUDA(cudaMemcpyAsync(crc_ok, d_crc, batch, cudaMemcpyDeviceToHost, cp));
   int32_t status = 0;
-  for (auto& s : plan->streams) NR_CUDA(cudaStreamSynchronize(s));
-  NR_CUDA(cudaMemcpy(&status, d_status, 4, cudaMemcpyDeviceToHost));
+  NR_CUDA(cudaMemcpyAsync(&status, d_status, 4, cudaMemcpyDeviceToHost, cp));
+  if (dbg) cudaEventRecord(t1, cp);
+  NR_CUDA(cudaStreamSynchronize(cp));
+  if (dbg) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, t0, t1);
+    fprintf(stderr, "decode_host gpu span %.3f ms\n", ms);
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+  }
   g_launches = launches;
   if (status) return fail(NRLDPC_EINVAL, "int8 LLR magnitudes must be at most 127");
   return NRLDPC_OK;
