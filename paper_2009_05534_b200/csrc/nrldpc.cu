@@ -61,11 +61,11 @@ struct GroupState {
 struct CtaState {
   int n_done;
   int n_valid;
-  int pad[2];
+  uint32_t kc[6];  // Consts, staged so every thread loads them once
 };
 
 constexpr int kLutBytes = 256;
-constexpr int kCtaBytes = 16;
+constexpr int kCtaBytes = 32;
 
 // k_decode_i8's shared layout: LUT, CTA state, group states, then per group
 // L and messages from this 16-aligned offset
@@ -182,6 +182,21 @@ __device__ __forceinline__ void two_smallest(const half2 (&t)[W], half2& m1, hal
 // tables; me0 is the row's first edge in this thread's shared-memory message
 // row. Split in two phases so that column-disjoint rows can be interleaved
 // in one basic block (process_rows2).
+// Per-kernel constants kept in registers for the whole decode. They are
+// staged through shared memory and loaded once, so ptxas keeps them live
+// instead of re-reading the constant bank in every layer unit.
+struct Consts {
+  uint32_t magic;       // 0x64646464: PRMT filler byte
+  uint32_t one;         // half2 {1.0, 1.0}
+  uint32_t bh, nd, cc;  // arithmetic beta rule (beta_h, -delta, C)
+};
+
+__device__ __forceinline__ uint32_t lds_u32(const uint32_t* a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"((uint32_t)__cvta_generic_to_shared(a)));
+  return v;
+}
+
 // ABS: the graph table's column bases are absolute shared-window addresses
 // (single-group CTAs); otherwise byte offsets from the group's L array.
 template <int MAXW, int LANES, bool REGMSG, bool ABS = false>
@@ -240,11 +255,11 @@ struct RowWork {
   // Split from the scatter so that fused rows share one branch on beta_mode
   // and their scatters stay in one basic block.
   half2 dd, b2s;  // (b1 - b2)' and b2'
-  __device__ __forceinline__ void beta_arith(const KParams& p, uint32_t one) {
+  __device__ __forceinline__ void beta_arith(const Consts& k) {
     // floor(beta*m) == RN(beta_h*(m - delta) + C) - C for every m in [0,127]
     // (verified exhaustively on the host); all FMA-pipe, no table lookups
-    const half2 sig = u2h((S & 0x80008000u) | one);
-    const half2 bh = u2h(p.beta_h), nd = u2h(p.ndelta_h), cc = u2h(p.c_h);
+    const half2 sig = u2h((S & 0x80008000u) | k.one);
+    const half2 bh = u2h(k.bh), nd = u2h(k.nd), cc = u2h(k.cc);
     const half2 B1 = __hfma2(__hadd2(m1, nd), bh, cc);
     const half2 B2 = __hfma2(__hadd2(m2, nd), bh, cc);
     dd = __hmul2(__hsub2(B1, B2), sig);
@@ -290,13 +305,12 @@ template <int MAXW, int LANES, bool REGMSG, bool ABS = false>
 __device__ __forceinline__ void process_row(const KParams& p, const uint32_t tb, const uint32_t mb, const int w,
                                             uint32_t zl, uint32_t ZL, uint8_t* __restrict__ Lg,
                                             uint8_t* __restrict__ Mz, uint32_t Mzs, uint32_t* mreg,
-                                            const uint16_t* __restrict__ lut, uint32_t magic,
-                                            uint32_t one, bool st_ok) {
+                                            const uint16_t* __restrict__ lut, const Consts& k, bool st_ok) {
   RowWork<MAXW, LANES, REGMSG, ABS> r;
-  r.gather(p, tb, mb, w, zl, ZL, Lg, Mz, Mzs, mreg, magic);
-  if (p.beta_mode) r.beta_arith(p, one);
-  else r.beta_lut(lut, one);
-  r.scatter(Lg, mreg, one, st_ok);
+  r.gather(p, tb, mb, w, zl, ZL, Lg, Mz, Mzs, mreg, k.magic);
+  if (p.beta_mode) r.beta_arith(k);
+  else r.beta_lut(lut, k.one);
+  r.scatter(Lg, mreg, k.one, st_ok);
 }
 
 // Two consecutive column-disjoint rows as one basic block: no barrier between
@@ -306,21 +320,20 @@ __device__ __forceinline__ void process_rows2(const KParams& p, uint32_t tba, ui
                                               uint32_t mbb,
                                               uint32_t zl, uint32_t ZL, uint8_t* __restrict__ Lg,
                                               uint8_t* __restrict__ Mz, uint32_t Mzs, uint32_t* mreg,
-                                              const uint16_t* __restrict__ lut, uint32_t magic,
-                                              uint32_t one, bool st_ok) {
+                                              const uint16_t* __restrict__ lut, const Consts& k, bool st_ok) {
   RowWork<WA, LANES, false, ABS> a;
   RowWork<WB, LANES, false, ABS> b;
-  a.gather(p, tba, mba, WA, zl, ZL, Lg, Mz, Mzs, mreg, magic);
-  b.gather(p, tbb, mbb, WB, zl, ZL, Lg, Mz, Mzs, mreg, magic);
+  a.gather(p, tba, mba, WA, zl, ZL, Lg, Mz, Mzs, mreg, k.magic);
+  b.gather(p, tbb, mbb, WB, zl, ZL, Lg, Mz, Mzs, mreg, k.magic);
   if (p.beta_mode) {
-    a.beta_arith(p, one);
-    b.beta_arith(p, one);
+    a.beta_arith(k);
+    b.beta_arith(k);
   } else {
-    a.beta_lut(lut, one);
-    b.beta_lut(lut, one);
+    a.beta_lut(lut, k.one);
+    b.beta_lut(lut, k.one);
   }
-  a.scatter(Lg, mreg, one, st_ok);
-  b.scatter(Lg, mreg, one, st_ok);
+  a.scatter(Lg, mreg, k.one, st_ok);
+  b.scatter(Lg, mreg, k.one, st_ok);
 }
 
 // Syndrome weight (decoder.py:323-329) and min|L| (decoder.py:480-483) over
@@ -372,7 +385,7 @@ struct RowCtx {
   uint8_t* Mz;
   uint32_t Ms;  // shared-window address of Mz
   const uint16_t* lut;
-  uint32_t magic, one;
+  Consts k;
   bool st_ok;
 };
 
@@ -494,7 +507,7 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
     for (int r = 0; r < p.rows; ++r) {
       const int e0 = p.row_start[r];
       process_row<MAXW, LANES, false>(p, p.tab_start[r] / 4u, (uint32_t)e0 * LANES, p.row_start[r + 1] - e0, c.zl, c.ZL, c.Lg, c.Mz, c.Ms,
-                                      rm.r4, c.lut, c.magic, c.one, c.st_ok);
+                                      rm.r4, c.lut, c.k, c.st_ok);
       if (p.bar_after[r]) __syncthreads();
     }
   } else {
@@ -502,19 +515,18 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
     if constexpr (NREG > 0) {
 #pragma unroll 1
       for (int r = 0; r < RegMsg<NREG>::nq; r += 2) {
-        process_row<19, LANES, true, ABS>(p, 5u * r, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.q[0], c.lut, c.magic,
-                                     c.one, c.st_ok);
+        process_row<19, LANES, true, ABS>(p, 5u * r, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.q[0], c.lut, c.k, c.st_ok);
         __syncthreads();
         process_row<19, LANES, true, ABS>(p, 5u * r + 5u, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.q[1], c.lut,
-                                     c.magic, c.one, c.st_ok);
+                                     c.k, c.st_ok);
         rm.rotate2();
         __syncthreads();
       }
       if constexpr (NREG == 6) {
-        process_row<3, LANES, true, ABS>(p, 20u, 0, 3, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r4, c.lut, c.magic, c.one,
+        process_row<3, LANES, true, ABS>(p, 20u, 0, 3, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r4, c.lut, c.k,
                                     c.st_ok);
         __syncthreads();
-        process_row<8, LANES, true, ABS>(p, 21u, 0, 8, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r5, c.lut, c.magic, c.one,
+        process_row<8, LANES, true, ABS>(p, 21u, 0, 8, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r5, c.lut, c.k,
                                     c.st_ok);
         __syncthreads();
       }
@@ -536,11 +548,10 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
       dispatch_unit<BG>(A.x, [&](auto WA, auto WB) {
         constexpr int wa = decltype(WA)::value, wb = decltype(WB)::value;
         if constexpr (wb == 0)
-          process_row<wa, LANES, false, ABS>(p, A.z, A.w, wa, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r4, c.lut, c.magic,
-                                             c.one, c.st_ok);
+          process_row<wa, LANES, false, ABS>(p, A.z, A.w, wa, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r4, c.lut, c.k, c.st_ok);
         else
           process_rows2<wa, wb, LANES, ABS>(p, A.z, A.w, B.x, B.y, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r4, c.lut,
-                                            c.magic, c.one, c.st_ok);
+                                            c.k, c.st_ok);
       });
       // consecutive column-disjoint rows form one layer: the next unit reads
       // no column this one wrote, so warps may run ahead into it
@@ -655,6 +666,11 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
     const long long rem = p.batch - first;
     cta->n_done = 0;
     cta->n_valid = (int)min(rem, (long long)p.groups * LANES);
+    cta->kc[0] = p.magic;
+    cta->kc[1] = p.one;
+    cta->kc[2] = p.beta_h;
+    cta->kc[3] = p.ndelta_h;
+    cta->kc[4] = p.c_h;
   }
   if (st_ok && z == 0) {
 #pragma unroll
@@ -727,9 +743,9 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
   }
   __syncthreads();
 
-  const uint32_t magic = p.magic;  // 0x64646464, opaque to ptxas
-  const uint32_t one = p.one;      // 0x3C003C00 (half2 1.0)
-  const RowCtx rc{zl, ZL, Lg, Mz, (uint32_t)__cvta_generic_to_shared(Mz), lut, magic, one, st_ok};
+  const Consts kc{lds_u32(&cta->kc[0]), lds_u32(&cta->kc[1]), lds_u32(&cta->kc[2]), lds_u32(&cta->kc[3]),
+                  lds_u32(&cta->kc[4])};
+  const RowCtx rc{zl, ZL, Lg, Mz, (uint32_t)__cvta_generic_to_shared(Mz), lut, kc, st_ok};
   RegMsg<NREG> rm;
   rm.init();
   for (int it = 1; it <= p.max_iter; ++it) {
