@@ -16,6 +16,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <bitset>
 #include <vector>
 
 #include "nrldpc_kernels.cuh"
@@ -301,21 +302,23 @@ struct RowWork {
   }
 };
 
-template <int MAXW, int LANES, bool REGMSG, bool ABS = false>
+// LUT: the beta rule may be the table (generic schedule); the compile-time
+// BG1/BG2 schedules are only used with the arithmetic rule (smaller bodies).
+template <int MAXW, int LANES, bool REGMSG, bool ABS = false, bool LUT = true>
 __device__ __forceinline__ void process_row(const KParams& p, const uint32_t tb, const uint32_t mb, const int w,
                                             uint32_t zl, uint32_t ZL, uint8_t* __restrict__ Lg,
                                             uint8_t* __restrict__ Mz, uint32_t Mzs, uint32_t* mreg,
                                             const uint16_t* __restrict__ lut, const Consts& k, bool st_ok) {
   RowWork<MAXW, LANES, REGMSG, ABS> r;
   r.gather(p, tb, mb, w, zl, ZL, Lg, Mz, Mzs, mreg, k.magic);
-  if (p.beta_mode) r.beta_arith(k);
+  if (!LUT || p.beta_mode) r.beta_arith(k);
   else r.beta_lut(lut, k.one);
   r.scatter(Lg, mreg, k.one, st_ok);
 }
 
 // Two consecutive column-disjoint rows as one basic block: no barrier between
 // them is needed and the scheduler interleaves their independent chains.
-template <int WA, int WB, int LANES, bool ABS = false>
+template <int WA, int WB, int LANES, bool ABS = false, bool LUT = true>
 __device__ __forceinline__ void process_rows2(const KParams& p, uint32_t tba, uint32_t mba, uint32_t tbb,
                                               uint32_t mbb,
                                               uint32_t zl, uint32_t ZL, uint8_t* __restrict__ Lg,
@@ -325,7 +328,7 @@ __device__ __forceinline__ void process_rows2(const KParams& p, uint32_t tba, ui
   RowWork<WB, LANES, false, ABS> b;
   a.gather(p, tba, mba, WA, zl, ZL, Lg, Mz, Mzs, mreg, k.magic);
   b.gather(p, tbb, mbb, WB, zl, ZL, Lg, Mz, Mzs, mreg, k.magic);
-  if (p.beta_mode) {
+  if (!LUT || p.beta_mode) {
     a.beta_arith(k);
     b.beta_arith(k);
   } else {
@@ -515,18 +518,18 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
     if constexpr (NREG > 0) {
 #pragma unroll 1
       for (int r = 0; r < RegMsg<NREG>::nq; r += 2) {
-        process_row<19, LANES, true, ABS>(p, 5u * r, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.q[0], c.lut, c.k, c.st_ok);
+        process_row<19, LANES, true, ABS, false>(p, 5u * r, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.q[0], c.lut, c.k, c.st_ok);
         __syncthreads();
-        process_row<19, LANES, true, ABS>(p, 5u * r + 5u, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.q[1], c.lut,
+        process_row<19, LANES, true, ABS, false>(p, 5u * r + 5u, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.q[1], c.lut,
                                      c.k, c.st_ok);
         rm.rotate2();
         __syncthreads();
       }
       if constexpr (NREG == 6) {
-        process_row<3, LANES, true, ABS>(p, 20u, 0, 3, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r4, c.lut, c.k,
+        process_row<3, LANES, true, ABS, false>(p, 20u, 0, 3, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r4, c.lut, c.k,
                                     c.st_ok);
         __syncthreads();
-        process_row<8, LANES, true, ABS>(p, 21u, 0, 8, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r5, c.lut, c.k,
+        process_row<8, LANES, true, ABS, false>(p, 21u, 0, 8, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r5, c.lut, c.k,
                                     c.st_ok);
         __syncthreads();
       }
@@ -548,9 +551,9 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
       dispatch_unit<BG>(A.x, [&](auto WA, auto WB) {
         constexpr int wa = decltype(WA)::value, wb = decltype(WB)::value;
         if constexpr (wb == 0)
-          process_row<wa, LANES, false, ABS>(p, A.z, A.w, wa, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r4, c.lut, c.k, c.st_ok);
+          process_row<wa, LANES, false, ABS, false>(p, A.z, A.w, wa, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r4, c.lut, c.k, c.st_ok);
         else
-          process_rows2<wa, wb, LANES, ABS>(p, A.z, A.w, B.x, B.y, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r4, c.lut,
+          process_rows2<wa, wb, LANES, ABS, false>(p, A.z, A.w, B.x, B.y, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r4, c.lut,
                                             c.k, c.st_ok);
       });
       // consecutive column-disjoint rows form one layer: the next unit reads
@@ -1509,15 +1512,15 @@ int nrldpc_plan_create(int device, int k_b, int z, int rows_used, const int32_t*
   // row since the last barrier (then r+1 can run concurrently with them).
   // Rows 0..5 keep their barriers (register-message rows are straight-line).
   {
-    uint64_t layer_cols = 0;
+    std::bitset<NR_MAX_BLOCKS> layer_cols;
     for (int r = 0; r < rows_used; ++r) {
-      for (int e = row_start[r]; e < row_start[r + 1]; ++e) layer_cols |= 1ull << cols[e];
-      uint64_t next = 0;
+      for (int e = row_start[r]; e < row_start[r + 1]; ++e) layer_cols.set(cols[e]);
+      std::bitset<NR_MAX_BLOCKS> next;
       if (r + 1 < rows_used)
-        for (int e = row_start[r + 1]; e < row_start[r + 2]; ++e) next |= 1ull << cols[e];
-      const bool disjoint = r + 1 < rows_used && r >= 6 && (next & layer_cols) == 0;
+        for (int e = row_start[r + 1]; e < row_start[r + 2]; ++e) next.set(cols[e]);
+      const bool disjoint = r + 1 < rows_used && r >= 6 && (next & layer_cols).none();
       kp.bar_after[r] = disjoint ? 0 : 1;
-      if (!disjoint) layer_cols = 0;
+      if (!disjoint) layer_cols.reset();
     }
   }
   // int8 beta rule: floor(beta * m) computed in float64 (decoder.py:208-212)
@@ -1531,7 +1534,9 @@ int nrldpc_plan_create(int device, int k_b, int z, int rows_used, const int32_t*
     bool same = true;
     for (int r = 0; r <= rows_used && same; ++r)
       same = row_start[r] == (bg == 1 ? RowW<1>::e0[r] : RowW<2>::e0[r]);
-    if (same) p->schedule = bg;
+    // the compile-time schedules carry only the arithmetic beta rule; a
+    // table-only beta decodes on the generic schedule
+    if (same && kp.beta_mode) p->schedule = bg;
   }
   // flooding: per column, its edges in row order (decoder.py:362-364)
   {

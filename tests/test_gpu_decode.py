@@ -142,6 +142,16 @@ def test_beta_values_vs_oracle(cuda_ok, beta):
     _oracle_cmp(bg, 46, nr.DecodeConfig(max_iter=15, beta=beta), oracle.quantize_i8(llr, 104))
 
 
+@pytest.mark.parametrize("bg_id,z,rows,beta", [("BG1", 384, 46, 0.7), ("BG2", 384, 42, 0.55),
+                                               ("BG1", 320, 20, 0.3)])
+def test_table_only_beta_large_z_vs_oracle(cuda_ok, bg_id, z, rows, beta):
+    """Betas without an exact half-arithmetic rule run the generic schedule
+    with the table rule; still bit-exact at the largest lifting sizes."""
+    bg = nr.load_basegraph(bg_id, z)
+    _, llr = noisy_llrs(bg, rows, 2.0, 6, seed=(z, rows))
+    _oracle_cmp(bg, rows, nr.DecodeConfig(max_iter=8, beta=beta), oracle.quantize_i8(llr, z))
+
+
 def test_trace_and_crc_vs_oracle(cuda_ok):
     bg = nr.load_basegraph("BG1", 64)
     params = nr.code_params(bg, 64, 46)
