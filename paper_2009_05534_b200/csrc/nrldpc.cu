@@ -438,14 +438,22 @@ __device__ __forceinline__ void dispatch_w(int w, F&& f) {
 // occur in the base graphs (BG1 rows 16..45, BG2 rows 11..41); the host
 // (build_units) fuses exactly these. The chain is ordered by how often each
 // unit occurs per iteration of the full graph.
-template <int BG, typename F>
+// NREG: rows 0..NREG-1 run from registers, so their weights (19 for the four
+// core rows, 3 for row 4) never reach the unit loop and get no body.
+template <int BG, int NREG, typename F>
 __device__ __forceinline__ void dispatch_unit(uint32_t code, F&& f) {
   const int c = (int)code;
 #define NR_U(a, b) else if (weq(c, (a) | ((b) << 8))) f(IC<a>{}, IC<b>{})
   if constexpr (BG == 1) {
     if (false) {}
     NR_U(5, 5); NR_U(5, 4); NR_U(7, 0); NR_U(6, 6); NR_U(6, 0); NR_U(4, 5); NR_U(9, 0); NR_U(6, 5);
-    NR_U(10, 0); NR_U(8, 0); NR_U(19, 0); NR_U(3, 0); NR_U(5, 0); NR_U(4, 0);
+    NR_U(10, 0); NR_U(8, 0); NR_U(5, 0); NR_U(4, 0);
+    if constexpr (NREG < 4) {
+      if (weq(c, 19)) f(IC<19>{}, IC<0>{});
+    }
+    if constexpr (NREG < 6) {
+      if (weq(c, 3)) f(IC<3>{}, IC<0>{});
+    }
   } else {
     if (false) {}
     NR_U(4, 4); NR_U(4, 0); NR_U(5, 0); NR_U(4, 3); NR_U(6, 0); NR_U(5, 4); NR_U(5, 3); NR_U(8, 0);
@@ -548,7 +556,7 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
       const uint2 B = nb;
       na = p.unit_a[u + 1];
       nb = p.unit_b[u + 1];
-      dispatch_unit<BG>(A.x, [&](auto WA, auto WB) {
+      dispatch_unit<BG, NREG>(A.x, [&](auto WA, auto WB) {
         constexpr int wa = decltype(WA)::value, wb = decltype(WB)::value;
         if constexpr (wb == 0)
           process_row<wa, LANES, false, ABS, false>(p, A.z, A.w, wa, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r4, c.lut, c.k, c.st_ok);
