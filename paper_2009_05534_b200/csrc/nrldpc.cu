@@ -620,6 +620,27 @@ __device__ __forceinline__ void write_bits(const KParams& p, const uint8_t* __re
   }
 }
 
+// The same with whole warps when Z % 32 == 0 (warps never straddle groups):
+// lane t of a warp reads position 32*w + t of both codewords with one
+// coalesced load and two ballots build the two packed words.
+template <int LANES>
+__device__ __forceinline__ void write_bits_warp(const KParams& p, const uint8_t* __restrict__ Lg, int z,
+                                                const int (&need)[2], long long cw0,
+                                                uint32_t* __restrict__ bits) {
+  const int K = p.k_b * p.z;
+  const int lid = z & 31;
+  for (int wi = z >> 5; wi < p.words; wi += p.z >> 5) {
+    const int pos = wi * 32 + lid;
+    const uint32_t u = pos < K ? ld_elem<LANES>(Lg + pos * LANES) : 0x8080u;
+    const uint32_t wa = __ballot_sync(0xFFFFFFFFu, (u & 0xFFu) < 128u);
+    const uint32_t wb = __ballot_sync(0xFFFFFFFFu, ((u >> 8) & 0xFFu) < 128u);
+    if (lid == 0) {
+      if (need[0]) bits[cw0 * p.words + wi] = wa;
+      if (LANES == 2 && need[1]) bits[(cw0 + 1) * p.words + wi] = wb;
+    }
+  }
+}
+
 // CRC over the K hard bits (codec.py:183-213) computed by the whole group.
 // The bit-serial register is linear over GF(2): after all K bits it equals
 // XOR over set bits i of rem(x^(K-1-i+L), g), tabulated on the host
@@ -803,9 +824,14 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
       for (int l = 0; l < LANES; ++l) fin[l] = lane_valid[l] && !gs.done[l] && !cand[l];
     }
     if (active) {
+      const int need[2] = {cand[0] || fin[0], LANES == 2 && (cand[1] || fin[1])};
+      if (p.z % 32 == 0) {
+        // group-uniform condition, whole warps per group: ballots are safe
+        if (need[0] || need[1]) write_bits_warp<LANES>(p, Lg, z, need, cw0, o.bits);
+      } else {
 #pragma unroll
-      for (int l = 0; l < LANES; ++l) {
-        if (cand[l] || fin[l]) write_bits<LANES>(p, Lg, z, l, cw0 + l, o.bits);
+        for (int l = 0; l < LANES; ++l)
+          if (need[l]) write_bits<LANES>(p, Lg, z, l, cw0 + l, o.bits);
       }
       if (z == 0) {
 #pragma unroll
