@@ -125,7 +125,9 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU baseline: the oracle port on the host cores
 
-def cpu_baseline(bg, rows, iters, threads: int, blocks: np.ndarray, k: int):
+def cpu_baseline(bg, rows, iters, threads: int, blocks: np.ndarray, k: int, gpu_out: dict | None = None):
+    """Times the oracle port on the host cores; its outputs double as the
+    parity check of the GPU decode of the same codewords (``gpu_out``)."""
     from oracle import oracle
     import paper_2009_05534_b200 as nr
     cfg = nr.DecodeConfig(max_iter=iters, early_stop="none")
@@ -133,11 +135,20 @@ def cpu_baseline(bg, rows, iters, threads: int, blocks: np.ndarray, k: int):
     sample = blocks[:n]
     oracle.decode(sample[: min(n, threads)], bg, cfg, threads=threads)  # warm
     t0 = time.perf_counter()
-    oracle.decode(sample, bg, cfg, threads=threads)
+    ref = oracle.decode(sample, bg, cfg, threads=threads)
     dt = time.perf_counter() - t0
-    return {"value": n * k / dt / 1e9, "unit": "Gbps", "cores": threads, "kind": "port",
+    line = {"value": n * k / dt / 1e9, "unit": "Gbps", "cores": threads, "kind": "port",
             "sample": f"{n} codewords of the same workload (BG1 Z=384, 10 iterations), "
                       f"oracle/ldpc_oracle.c over {threads} OpenMP threads, {dt:.2f} s wall"}
+    if gpu_out is not None:
+        bits = nr.unpack_bits(gpu_out["bits"][:n], k)
+        same = (np.array_equal(bits, ref["bits"])
+                and np.array_equal(gpu_out["iters"][:n], ref["iterations"])
+                and np.array_equal(gpu_out["synd"][:n], ref["syndrome_weight"])
+                and np.array_equal(gpu_out["success"][:n].astype(bool), ref["success"]))
+        line["parity"] = {"codewords": n, "bit_exact": bool(same),
+                          "vs": "oracle (pinned to the reference's golden vectors)"}
+    return line
 
 
 def host_threads(requested: int) -> int:
@@ -235,7 +246,8 @@ def run_ours(args):
     # correctness / BLER of one decode (outside the timed region)
     plan.decode_device(bufs[0], outs[0])
     torch.cuda.synchronize(dev)
-    bits = nr.unpack_bits(outs[0]["bits"].cpu().numpy(), k)
+    gpu_host = {key: outs[0][key].cpu().numpy() for key in ("bits", "iters", "synd", "success")}
+    bits = nr.unpack_bits(gpu_host["bits"], k)
     bler = float((bits != msgs).any(axis=1).mean())
     success = float(outs[0]["success"].float().mean().item())
     # the same inputs with the reference's syndrome early stop (quality check;
@@ -374,7 +386,7 @@ def run_ours(args):
 
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = host_threads(args.cpu_threads)
-        line["cpu_baseline"] = cpu_baseline(bg, rows, args.iters, threads, blocks0.cpu().numpy(), k)
+        line["cpu_baseline"] = cpu_baseline(bg, rows, args.iters, threads, blocks0.cpu().numpy(), k, gpu_host)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
