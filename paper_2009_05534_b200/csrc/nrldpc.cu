@@ -202,12 +202,17 @@ __device__ __forceinline__ uint32_t lds_u32(const uint32_t* a) {
 // (single-group CTAs); otherwise byte offsets from the group's L array.
 template <int MAXW, int LANES, bool REGMSG, bool ABS = false>
 struct RowWork {
+  // ABS pair shapes store a row's messages two edges per 32-bit word (one
+  // LDS.32 / STS.32 per two edges); an odd row's last edge sits in a
+  // half-word slot shared with another odd row (Mh). Host: msg_layout().
+  static constexpr bool PAIRED = ABS && LANES == 2 && !REGMSG;
   uint32_t off[MAXW];
   half2 t[MAXW];
   half2 m1, m2;
   uint32_t S;
   uint8_t* Mrow;
   uint32_t Ms;  // ABS: shared-window address of Mrow
+  uint32_t Mh;  // PAIRED: shared-window address of the odd edge's slot
   int w;
 
   // phase 1: gather L and the old messages, t = L - M, fold (m1, m2, S)
@@ -216,23 +221,40 @@ struct RowWork {
   __device__ __forceinline__ void gather(const KParams& p, const uint32_t tb, const uint32_t mb, const int w_,
                                          uint32_t zl, uint32_t ZL, const uint8_t* __restrict__ Lg,
                                          uint8_t* __restrict__ Mz, uint32_t Mzs, const uint32_t* mreg,
-                                         uint32_t magic) {
+                                         uint32_t magic, uint32_t mh_off = 0) {
     const half2 H127 = u2h(0x57F057F0u);
     w = w_;
     Mrow = Mz + mb;
     Ms = Mzs + mb;
+    Mh = Mzs + mh_off;
     uint32_t tsh[MAXW], tcb[MAXW];
     load_row_tables<MAXW>(p, tb, w, tsh, tcb);
     m1 = H127;
     m2 = H127;
     S = 0;
+    uint32_t mw[(MAXW + 1) / 2];
+    if constexpr (PAIRED) {
+#pragma unroll
+      for (int i = 0; i < MAXW / 2; ++i)
+        if (2 * i + 1 < w) mw[i] = lds_u32(Ms + 4 * i);
+      // (paired rows always run with w == MAXW: compile-time row bodies)
+      if (MAXW & 1) mw[MAXW / 2] = lds_elem<2>(Mh);
+    }
 #pragma unroll
     for (int j = 0; j < MAXW; ++j) {
       if (j < w) {
         off[j] = edge_offset(tsh[j], tcb[j], zl, ZL);
         const uint32_t raw = ABS ? lds_elem<LANES>(off[j]) : ld_elem<LANES>(Lg + off[j]);
         const half2 lh = unpack_elem<LANES>(raw, magic);
-        const half2 mh = msg_load<LANES, REGMSG, ABS>(Mrow, Ms, mreg, j, j, magic);
+        half2 mh;
+        if constexpr (PAIRED) {
+          uint32_t d;
+          if (j & 1) asm("prmt.b32 %0, %1, %2, 0x4342;" : "=r"(d) : "r"(mw[j >> 1]), "r"(magic));
+          else asm("prmt.b32 %0, %1, %2, 0x4140;" : "=r"(d) : "r"(mw[j >> 1]), "r"(magic));
+          mh = u2h(d);
+        } else {
+          mh = msg_load<LANES, REGMSG, ABS>(Mrow, Ms, mreg, j, j, magic);
+        }
         const half2 tj = __hsub2(lh, mh);           // exact: L - M
         S ^= h2u(tj);                               // sign product (bits 15/31)
         t[j] = tj;
@@ -296,10 +318,19 @@ struct RowWork {
         const uint32_t lnew = pack_elem<LANES>(__hfma2(y, sg, H1152));
         if constexpr (ABS) sts_elem_if<LANES>(off[j], lnew, st_ok);
         else st_elem_if<LANES>(Lg + off[j], lnew, st_ok);
-        msg_store<LANES, REGMSG, ABS>(Mrow, Ms, mreg, j, j, __hfma2(mag, sg, H1152), st_ok);
+        const half2 mb = __hfma2(mag, sg, H1152);
+        if constexpr (PAIRED) {
+          // two edges' biased messages -> one word: low bytes of each half
+          if (j & 1) sts_u32_if(Ms + 4 * (j >> 1), __byte_perm(h2u(mprev), h2u(mb), 0x6420), st_ok);
+          else if (j == w - 1) sts_elem_if<2>(Mh, pack_elem<2>(mb), st_ok);
+          mprev = mb;
+        } else {
+          msg_store<LANES, REGMSG, ABS>(Mrow, Ms, mreg, j, j, mb, st_ok);
+        }
       }
     }
   }
+  half2 mprev;
 };
 
 // LUT: the beta rule may be the table (generic schedule); the compile-time
@@ -308,9 +339,10 @@ template <int MAXW, int LANES, bool REGMSG, bool ABS = false, bool LUT = true>
 __device__ __forceinline__ void process_row(const KParams& p, const uint32_t tb, const uint32_t mb, const int w,
                                             uint32_t zl, uint32_t ZL, uint8_t* __restrict__ Lg,
                                             uint8_t* __restrict__ Mz, uint32_t Mzs, uint32_t* mreg,
-                                            const uint16_t* __restrict__ lut, const Consts& k, bool st_ok) {
+                                            const uint16_t* __restrict__ lut, const Consts& k, bool st_ok,
+                                            uint32_t mh = 0) {
   RowWork<MAXW, LANES, REGMSG, ABS> r;
-  r.gather(p, tb, mb, w, zl, ZL, Lg, Mz, Mzs, mreg, k.magic);
+  r.gather(p, tb, mb, w, zl, ZL, Lg, Mz, Mzs, mreg, k.magic, mh);
   if (!LUT || p.beta_mode) r.beta_arith(k);
   else r.beta_lut(lut, k.one);
   r.scatter(Lg, mreg, k.one, st_ok);
@@ -323,11 +355,12 @@ __device__ __forceinline__ void process_rows2(const KParams& p, uint32_t tba, ui
                                               uint32_t mbb,
                                               uint32_t zl, uint32_t ZL, uint8_t* __restrict__ Lg,
                                               uint8_t* __restrict__ Mz, uint32_t Mzs, uint32_t* mreg,
-                                              const uint16_t* __restrict__ lut, const Consts& k, bool st_ok) {
+                                              const uint16_t* __restrict__ lut, const Consts& k, bool st_ok,
+                                              uint32_t mha = 0, uint32_t mhb = 0) {
   RowWork<WA, LANES, false, ABS> a;
   RowWork<WB, LANES, false, ABS> b;
-  a.gather(p, tba, mba, WA, zl, ZL, Lg, Mz, Mzs, mreg, k.magic);
-  b.gather(p, tbb, mbb, WB, zl, ZL, Lg, Mz, Mzs, mreg, k.magic);
+  a.gather(p, tba, mba, WA, zl, ZL, Lg, Mz, Mzs, mreg, k.magic, mha);
+  b.gather(p, tbb, mbb, WB, zl, ZL, Lg, Mz, Mzs, mreg, k.magic, mhb);
   if (!LUT || p.beta_mode) {
     a.beta_arith(k);
     b.beta_arith(k);
@@ -549,20 +582,21 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
     // ahead so the dispatch after a barrier does not wait on the constant
     // cache.
     uint4 na = p.unit_a[0];
-    uint2 nb = p.unit_b[0];
+    uint4 nb = p.unit_b[0];
 #pragma unroll 1
     for (int u = 0; u < p.n_units; ++u) {
       const uint4 A = na;
-      const uint2 B = nb;
+      const uint4 B = nb;
       na = p.unit_a[u + 1];
       nb = p.unit_b[u + 1];
       dispatch_unit<BG, NREG>(A.x, [&](auto WA, auto WB) {
         constexpr int wa = decltype(WA)::value, wb = decltype(WB)::value;
         if constexpr (wb == 0)
-          process_row<wa, LANES, false, ABS, false>(p, A.z, A.w, wa, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r4, c.lut, c.k, c.st_ok);
+          process_row<wa, LANES, false, ABS, false>(p, A.z, A.w, wa, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r4, c.lut, c.k,
+                                                    c.st_ok, B.z);
         else
           process_rows2<wa, wb, LANES, ABS, false>(p, A.z, A.w, B.x, B.y, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r4, c.lut,
-                                            c.k, c.st_ok);
+                                                   c.k, c.st_ok, B.z, B.w);
       });
       // consecutive column-disjoint rows form one layer: the next unit reads
       // no column this one wrote, so warps may run ahead into it
@@ -955,7 +989,7 @@ struct Shape {
   int lanes = 1;    // codewords per half2 lane pair
   int nreg = 0;     // leading rows whose messages live in registers (BG1 pairs)
   int groups = 1;   // codeword groups (of Z threads) per CTA
-  int threads = 32;
+  int threads = 0;  // 0: no feasible shape
   size_t smem = 0;
   int occ = 0;      // resident CTAs per SM (0: not queried yet)
   bool abs = false; // kp.cb holds absolute shared-window addresses
@@ -1154,30 +1188,69 @@ bool fused_pair(int schedule, int wa, int wb) {
 }
 
 // Layer units for rows nreg.. of a BG1/BG2 kernel (see KParams::unit_a).
-void build_units(const nrldpc_plan* p, int nreg, int e_reg, int lanes, KParams& kp) {
+// Per-thread shared-memory message slots of rows nreg.. (byte offsets).
+// Edge-ordered: row r's edges at (row_start[r] - e_reg) * lanes. Paired (ABS
+// pair shapes): each row's first 2*floor(w/2) edges as whole 32-bit words;
+// the last edge of an odd row takes half of a word whose other half holds
+// another odd row's last edge. Returns the slot count in edges.
+struct MsgLayout {
+  uint32_t mb[NR_MAX_ROWS];  // first (paired) slot
+  uint32_t mh[NR_MAX_ROWS];  // odd edge's half-word slot (paired only)
+  int slots = 0;
+};
+
+MsgLayout msg_layout(const nrldpc_plan* p, int nreg, int e_reg, int lanes, bool paired) {
+  const KParams& b = p->base;
+  MsgLayout m{};
+  if (!paired) {
+    for (int r = nreg; r < p->rows; ++r) m.mb[r] = (uint32_t)(b.row_start[r] - e_reg) * lanes;
+    m.slots = b.row_start[p->rows] - e_reg;
+    return m;
+  }
+  int cur = 0, free_half = -1;  // in edge slots (2 bytes each)
+  for (int r = nreg; r < p->rows; ++r) {
+    const int w = b.row_start[r + 1] - b.row_start[r];
+    m.mb[r] = (uint32_t)cur * 2u;
+    cur += 2 * (w / 2);
+    if (w & 1) {
+      if (free_half >= 0) {
+        m.mh[r] = (uint32_t)free_half * 2u;
+        free_half = -1;
+      } else {
+        m.mh[r] = (uint32_t)cur * 2u;
+        free_half = cur + 1;
+        cur += 2;
+      }
+    }
+  }
+  m.slots = cur;
+  return m;
+}
+
+void build_units(const nrldpc_plan* p, int nreg, const MsgLayout& ml, KParams& kp) {
   const KParams& b = p->base;
   int n = 0;
   for (int r = nreg; r < p->rows;) {
     const int wa = b.row_start[r + 1] - b.row_start[r];
-    const uint32_t ta = b.tab_start[r] / 4u, ma = (uint32_t)(b.row_start[r] - e_reg) * lanes;
+    const uint32_t ta = b.tab_start[r] / 4u;
     if (p->schedule != 0 && !b.bar_after[r] && r + 1 < p->rows) {
       const int wb = b.row_start[r + 2] - b.row_start[r + 1];
       if (fused_pair(p->schedule, wa, wb)) {
-        kp.unit_a[n] = make_uint4((uint32_t)(wa | wb << 8), b.bar_after[r + 1], ta, ma);
-        kp.unit_b[n] = make_uint2(b.tab_start[r + 1] / 4u, (uint32_t)(b.row_start[r + 1] - e_reg) * lanes);
+        kp.unit_a[n] = make_uint4((uint32_t)(wa | wb << 8), b.bar_after[r + 1], ta, ml.mb[r]);
+        kp.unit_b[n] = make_uint4(b.tab_start[r + 1] / 4u, ml.mb[r + 1], ml.mh[r], ml.mh[r + 1]);
         ++n;
         r += 2;
         continue;
       }
     }
-    kp.unit_a[n] = make_uint4((uint32_t)wa, b.bar_after[r], ta, ma);
-    kp.unit_b[n] = make_uint2(0, 0);
+    kp.unit_a[n] = make_uint4((uint32_t)wa, b.bar_after[r], ta, ml.mb[r]);
+    kp.unit_b[n] = make_uint4(0, 0, ml.mh[r], 0);
     ++n;
     r += 1;
   }
   kp.n_units = n;
   kp.unit_a[n] = make_uint4(0, 0, 0, 0);
-  kp.unit_b[n] = make_uint2(0, 0);
+  kp.unit_b[n] = make_uint4(0, 0, 0, 0);
 }
 
 Shape choose_shape(const nrldpc_plan* p, int max_lanes) {
@@ -1210,8 +1283,8 @@ Shape choose_shape(const nrldpc_plan* p, int max_lanes) {
   }
   const int e_reg = nreg ? RowW<1>::e0[nreg] : 0;
   const size_t lb = align16(n_pos * lanes);
-  const size_t e_pad = padded_edges(p->n_edges - e_reg, lanes);
-  const size_t mb = msg_bytes(lanes, e_reg);
+  size_t e_pad = padded_edges(p->n_edges - e_reg, lanes);
+  size_t mb = msg_bytes(lanes, e_reg);
   int best_g = 1;
   double best_waste = 1e9;
   const int max_thr = nreg ? 384 : 512;
@@ -1227,6 +1300,28 @@ Shape choose_shape(const nrldpc_plan* p, int max_lanes) {
     }
     if (waste <= 1.0 / 16) break;
   }
+  // single-group pair shapes of the BG1/BG2 schedules address L absolutely:
+  // the table holds column base + the L array's shared-window address (the
+  // dynamic window starts after the 1 KB system reservation; the kernel
+  // verifies), and their messages use the paired word layout.
+  // Absolute L addressing is ~5% faster for one decode alone, but measured
+  // ~12% slower when many plans' kernels share the SMs (mixed-shape batches,
+  // nrldpc_plan_set_coscheduled); register-row shapes always use it.
+  bool abs = best_g == 1 && lanes == 2 && p->schedule != 0 && (nreg > 0 || !p->coscheduled);
+  MsgLayout ml = msg_layout(p, nreg, e_reg, lanes, abs);
+  if (abs) {
+    const size_t e_pad_p = padded_edges(ml.slots, lanes);
+    const size_t mb_p = align16((size_t)p->z * e_pad_p * lanes);
+    if (smem_for(1, lb, mb_p) <= smem_max) {
+      e_pad = e_pad_p;
+      mb = mb_p;
+    } else if (nreg == 0) {
+      abs = false;
+      ml = msg_layout(p, nreg, e_reg, lanes, false);
+    } else {
+      return Shape{};  // no feasible layout (threads == 0: plan creation fails)
+    }
+  }
   Shape sh;
   sh.lanes = lanes;
   sh.nreg = nreg;
@@ -1239,17 +1334,9 @@ Shape choose_shape(const nrldpc_plan* p, int max_lanes) {
   sh.kp.m_bytes = (uint32_t)mb;
   sh.kp.m_stride = (uint32_t)(e_pad * lanes);
   sh.kp.e_reg = e_reg;
-  build_units(p, nreg, e_reg, lanes, sh.kp);
+  build_units(p, nreg, ml, sh.kp);
   sh.kp.magic = 0x64646464u;
   sh.kp.one = 0x3C003C00u;
-  // single-group pair shapes of the BG1/BG2 schedules address L absolutely:
-  // the table holds column base + the L array's shared-window address (the
-  // dynamic window starts after the 1 KB system reservation; the kernel
-  // verifies)
-  // Absolute L addressing is ~5% faster for one decode alone, but measured
-  // ~12% slower when many plans' kernels share the SMs (mixed-shape batches,
-  // nrldpc_plan_set_coscheduled); register-row shapes always use it.
-  const bool abs = best_g == 1 && lanes == 2 && p->schedule != 0 && (nreg > 0 || !p->coscheduled);
   sh.kp.abs_base = abs ? kSmemWindowBase + data_offset(1) : 0u;
   sh.abs = sh.kp.abs_base != 0;
   for (int t = 0; t < NR_MAX_TAB; ++t) {
@@ -1263,6 +1350,7 @@ Shape choose_shape(const nrldpc_plan* p, int max_lanes) {
 
 static cudaError_t launch_shape(const nrldpc_plan* plan, Shape& sh, const int8_t* in, int64_t batch,
                                 const KOut& o, cudaStream_t st) {
+  if (sh.threads == 0) return cudaErrorInvalidConfiguration;  // no feasible shape
   const bool two = sh.lanes == 2;
   const int dev = plan->device;
   switch (plan->schedule) {

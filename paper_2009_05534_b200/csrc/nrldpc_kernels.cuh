@@ -60,11 +60,12 @@ struct alignas(16) KParams {
   uint8_t bar_after[NR_MAX_ROWS];       // 0: next row is column-disjoint from this layer
   // layer units of the BG1/BG2 kernels after the register rows (one row or
   // two fused column-disjoint rows): a = {code wa | wb << 8, barrier after,
-  // table slot / 4 of row a, message byte offset of row a}, b = the same
-  // offsets of row b. One spare entry for the one-ahead prefetch.
+  // table slot / 4 of row a, message byte offset of row a}, b = {table slot
+  // / 4 of row b, message byte offset of row b, odd-edge slot offsets of rows
+  // a and b (paired message layout)}. One spare entry for the prefetch.
   int n_units;
   alignas(16) uint4 unit_a[NR_MAX_ROWS + 1];
-  alignas(8) uint2 unit_b[NR_MAX_ROWS + 1];
+  alignas(16) uint4 unit_b[NR_MAX_ROWS + 1];
   // per-edge graph tables, each row padded to a multiple of 4 slots so a row
   // loads them with 128-bit uniform constant loads
   alignas(16) uint32_t sh[NR_MAX_TAB];  // shift * LANES (bytes)
@@ -158,6 +159,17 @@ __device__ __forceinline__ void sts_elem_if(uint32_t a, uint32_t v, bool ok) {
   else
     asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.u8 [%0], %1; }" ::"r"(a), "h"((uint16_t)v),
                  "r"((uint32_t)ok));
+}
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+
+__device__ __forceinline__ void sts_u32_if(uint32_t a, uint32_t v, bool ok) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.u32 [%0], %1; }" ::"r"(a), "r"(v),
+               "r"((uint32_t)ok));
 }
 
 // beta LUT on a half2 of integer magnitudes 0..127
