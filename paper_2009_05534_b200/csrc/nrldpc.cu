@@ -582,13 +582,13 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
     // ahead so the dispatch after a barrier does not wait on the constant
     // cache.
     uint4 na = p.unit_a[0];
-    uint4 nb = p.unit_b[0];
 #pragma unroll 1
     for (int u = 0; u < p.n_units; ++u) {
+      // only the dispatch word set is prefetched (fewer loop-carried copies);
+      // the second half is needed later in the body
       const uint4 A = na;
-      const uint4 B = nb;
+      const uint4 B = p.unit_b[u];
       na = p.unit_a[u + 1];
-      nb = p.unit_b[u + 1];
       dispatch_unit<BG, NREG>(A.x, [&](auto WA, auto WB) {
         constexpr int wa = decltype(WA)::value, wb = decltype(WB)::value;
         if constexpr (wb == 0)
