@@ -215,24 +215,23 @@ struct RowWork {
   uint32_t Mh;  // PAIRED: shared-window address of the odd edge's slot
   int w;
 
-  // phase 1: gather L and the old messages, t = L - M, fold (m1, m2, S)
+  // phase 1: gather L and the old messages, t = L - M, fold (m1, m2, S).
+  // Split in two: gather_pro touches only this thread's own state (graph
+  // tables, edge addresses, its messages), so it may run before the layer
+  // barrier that orders the previous layer's posterior stores; gather_main
+  // reads the posteriors.
   // tb: the row's table slot / 4; mb: byte offset of its first
   // message in this thread's shared-memory message row
-  __device__ __forceinline__ void gather(const KParams& p, const uint32_t tb, const uint32_t mb, const int w_,
-                                         uint32_t zl, uint32_t ZL, const uint8_t* __restrict__ Lg,
-                                         uint8_t* __restrict__ Mz, uint32_t Mzs, const uint32_t* mreg,
-                                         uint32_t magic, uint32_t mh_off = 0) {
-    const half2 H127 = u2h(0x57F057F0u);
+  uint32_t mw[(MAXW + 1) / 2];
+  __device__ __forceinline__ void gather_pro(const KParams& p, const uint32_t tb, const uint32_t mb, const int w_,
+                                             uint32_t zl, uint32_t ZL, uint8_t* __restrict__ Mz, uint32_t Mzs,
+                                             uint32_t mh_off) {
     w = w_;
     Mrow = Mz + mb;
     Ms = Mzs + mb;
     Mh = Mzs + mh_off;
     uint32_t tsh[MAXW], tcb[MAXW];
     load_row_tables<MAXW>(p, tb, w, tsh, tcb);
-    m1 = H127;
-    m2 = H127;
-    S = 0;
-    uint32_t mw[(MAXW + 1) / 2];
     if constexpr (PAIRED) {
 #pragma unroll
       for (int i = 0; i < MAXW / 2; ++i)
@@ -241,9 +240,18 @@ struct RowWork {
       if (MAXW & 1) mw[MAXW / 2] = lds_elem<2>(Mh);
     }
 #pragma unroll
+    for (int j = 0; j < MAXW; ++j)
+      if (j < w) off[j] = edge_offset(tsh[j], tcb[j], zl, ZL);
+  }
+  __device__ __forceinline__ void gather_main(const uint8_t* __restrict__ Lg, const uint32_t* mreg,
+                                              uint32_t magic) {
+    const half2 H127 = u2h(0x57F057F0u);
+    m1 = H127;
+    m2 = H127;
+    S = 0;
+#pragma unroll
     for (int j = 0; j < MAXW; ++j) {
       if (j < w) {
-        off[j] = edge_offset(tsh[j], tcb[j], zl, ZL);
         const uint32_t raw = ABS ? lds_elem<LANES>(off[j]) : ld_elem<LANES>(Lg + off[j]);
         const half2 lh = unpack_elem<LANES>(raw, magic);
         half2 mh;
@@ -272,6 +280,14 @@ struct RowWork {
         }
       }
     }
+  }
+  __device__ __forceinline__ void gather(const KParams& p, const uint32_t tb, const uint32_t mb, const int w_,
+                                         uint32_t zl, uint32_t ZL, const uint8_t* __restrict__ Lg,
+                                         uint8_t* __restrict__ Mz, uint32_t Mzs, const uint32_t* mreg,
+                                         uint32_t magic, uint32_t mh_off = 0, bool bar = false) {
+    gather_pro(p, tb, mb, w_, zl, ZL, Mz, Mzs, mh_off);
+    if (bar) __syncthreads();
+    gather_main(Lg, mreg, magic);
   }
 
   // beta-scaled magnitudes with the row sign folded in: b' = (-1)^S * b.
@@ -340,9 +356,9 @@ __device__ __forceinline__ void process_row(const KParams& p, const uint32_t tb,
                                             uint32_t zl, uint32_t ZL, uint8_t* __restrict__ Lg,
                                             uint8_t* __restrict__ Mz, uint32_t Mzs, uint32_t* mreg,
                                             const uint16_t* __restrict__ lut, const Consts& k, bool st_ok,
-                                            uint32_t mh = 0) {
+                                            uint32_t mh = 0, bool bar = false) {
   RowWork<MAXW, LANES, REGMSG, ABS> r;
-  r.gather(p, tb, mb, w, zl, ZL, Lg, Mz, Mzs, mreg, k.magic, mh);
+  r.gather(p, tb, mb, w, zl, ZL, Lg, Mz, Mzs, mreg, k.magic, mh, bar);
   if (!LUT || p.beta_mode) r.beta_arith(k);
   else r.beta_lut(lut, k.one);
   r.scatter(Lg, mreg, k.one, st_ok);
@@ -356,11 +372,14 @@ __device__ __forceinline__ void process_rows2(const KParams& p, uint32_t tba, ui
                                               uint32_t zl, uint32_t ZL, uint8_t* __restrict__ Lg,
                                               uint8_t* __restrict__ Mz, uint32_t Mzs, uint32_t* mreg,
                                               const uint16_t* __restrict__ lut, const Consts& k, bool st_ok,
-                                              uint32_t mha = 0, uint32_t mhb = 0) {
+                                              uint32_t mha = 0, uint32_t mhb = 0, bool bar = false) {
   RowWork<WA, LANES, false, ABS> a;
   RowWork<WB, LANES, false, ABS> b;
-  a.gather(p, tba, mba, WA, zl, ZL, Lg, Mz, Mzs, mreg, k.magic, mha);
-  b.gather(p, tbb, mbb, WB, zl, ZL, Lg, Mz, Mzs, mreg, k.magic, mhb);
+  a.gather_pro(p, tba, mba, WA, zl, ZL, Mz, Mzs, mha);
+  b.gather_pro(p, tbb, mbb, WB, zl, ZL, Mz, Mzs, mhb);
+  if (bar) __syncthreads();
+  a.gather_main(Lg, mreg, k.magic);
+  b.gather_main(Lg, mreg, k.magic);
   if (!LUT || p.beta_mode) {
     a.beta_arith(k);
     b.beta_arith(k);
@@ -582,6 +601,11 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
     // ahead so the dispatch after a barrier does not wait on the constant
     // cache.
     uint4 na = p.unit_a[0];
+    // The barrier that closes a layer runs inside the next unit, after its
+    // thread-private prologue (tables, addresses, own messages) and before
+    // its first posterior load, so warps arriving early do useful work.
+    // The register rows above end with their own barrier.
+    bool bar_prev = false;
 #pragma unroll 1
     for (int u = 0; u < p.n_units; ++u) {
       // only the dispatch word set is prefetched (fewer loop-carried copies);
@@ -593,15 +617,16 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
         constexpr int wa = decltype(WA)::value, wb = decltype(WB)::value;
         if constexpr (wb == 0)
           process_row<wa, LANES, false, ABS, false>(p, A.z, A.w, wa, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r4, c.lut, c.k,
-                                                    c.st_ok, B.z);
+                                                    c.st_ok, B.z, bar_prev);
         else
           process_rows2<wa, wb, LANES, ABS, false>(p, A.z, A.w, B.x, B.y, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r4, c.lut,
-                                                   c.k, c.st_ok, B.z, B.w);
+                                                   c.k, c.st_ok, B.z, B.w, bar_prev);
       });
       // consecutive column-disjoint rows form one layer: the next unit reads
       // no column this one wrote, so warps may run ahead into it
-      if (A.y) __syncthreads();
+      bar_prev = A.y != 0;
     }
+    if (bar_prev) __syncthreads();
   }
 }
 
