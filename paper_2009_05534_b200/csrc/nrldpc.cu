@@ -574,26 +574,25 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
       if (p.bar_after[r]) __syncthreads();
     }
   } else {
-    int r0 = 0;
+    bool bar_prev = false;  // a layer barrier is owed before the next posterior load
     if constexpr (NREG > 0) {
+      // each row runs its table/address prologue before the barrier that
+      // closes the previous row (the iteration starts after a barrier)
 #pragma unroll 1
       for (int r = 0; r < RegMsg<NREG>::nq; r += 2) {
-        process_row<19, LANES, true, ABS, false>(p, 5u * r, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.q[0], c.lut, c.k, c.st_ok);
-        __syncthreads();
+        process_row<19, LANES, true, ABS, false>(p, 5u * r, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.q[0], c.lut, c.k,
+                                                 c.st_ok, 0, r != 0);
         process_row<19, LANES, true, ABS, false>(p, 5u * r + 5u, 0, 19, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.q[1], c.lut,
-                                     c.k, c.st_ok);
+                                                 c.k, c.st_ok, 0, true);
         rm.rotate2();
-        __syncthreads();
       }
       if constexpr (NREG == 6) {
         process_row<3, LANES, true, ABS, false>(p, 20u, 0, 3, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r4, c.lut, c.k,
-                                    c.st_ok);
-        __syncthreads();
+                                                c.st_ok, 0, true);
         process_row<8, LANES, true, ABS, false>(p, 21u, 0, 8, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r5, c.lut, c.k,
-                                    c.st_ok);
-        __syncthreads();
+                                                c.st_ok, 0, true);
       }
-      r0 = NREG;
+      bar_prev = true;
     }
     // The remaining rows run as host-built units (a single row, or two
     // consecutive column-disjoint rows fused into one basic block) with
@@ -604,8 +603,6 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
     // The barrier that closes a layer runs inside the next unit, after its
     // thread-private prologue (tables, addresses, own messages) and before
     // its first posterior load, so warps arriving early do useful work.
-    // The register rows above end with their own barrier.
-    bool bar_prev = false;
 #pragma unroll 1
     for (int u = 0; u < p.n_units; ++u) {
       // only the dispatch word set is prefetched (fewer loop-carried copies);
