@@ -627,10 +627,19 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
   }
 }
 
+// early: only "any unsatisfied check" matters (an early-stop iteration that
+// is neither traced nor the last). A warp then stops scanning rows once it
+// holds a failing check of every lane still being decoded (need_a/need_b):
+// one failure anywhere in the group already rules the codeword out. Only
+// when warps never straddle groups (Z % 32 == 0). wcnt is then a lower
+// bound of the weight (>0 iff some check fails), and mabs is left at 255 for
+// lanes known to fail.
 template <int BG, int MAXW, int LANES, bool ABS>
 __device__ __forceinline__ void local_check(const KParams& p, uint32_t zl, uint32_t ZL,
-                                            const uint8_t* __restrict__ Lg, int* wcnt, int* mabs) {
+                                            const uint8_t* __restrict__ Lg, int* wcnt, int* mabs,
+                                            bool early = false, bool need_a = true, bool need_b = true) {
   int wa = 0, wb = 0;
+  bool stopped = false;
   if constexpr (BG == 0) {
     for (int r = 0; r < p.rows; ++r) {
       const int e0 = p.row_start[r];
@@ -644,10 +653,18 @@ __device__ __forceinline__ void local_check(const KParams& p, uint32_t zl, uint3
       dispatch_w<BG>(p.row_start[r + 1] - e0, [&](auto W) {
         row_parity<decltype(W)::value, LANES, ABS>(p, t0 / 4u, decltype(W)::value, zl, ZL, Lg, wa, wb);
       });
+      if (early) {
+        const bool fa = !need_a || __any_sync(0xFFFFFFFFu, wa != 0);
+        const bool fb = LANES == 1 || !need_b || __any_sync(0xFFFFFFFFu, wb != 0);
+        if (fa && fb) {
+          stopped = true;
+          break;
+        }
+      }
     }
   }
   int ma = 255, mb = 255;
-  for (int c = 0; c < p.n_blocks; ++c) {
+  for (int c = 0; c < p.n_blocks && !stopped; ++c) {
     const uint32_t u = ld_elem<LANES>(Lg + (uint32_t)c * ZL + zl);
     ma = min(ma, abs((int)(u & 0xFFu) - 128));
     mb = min(mb, abs((int)((u >> 8) & 0xFFu) - 128));
@@ -844,7 +861,10 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
     // ---- end-of-iteration check (decoder.py:497-536) ----
     {
       int wc[2], ma[2];
-      local_check<BG, MAXW, LANES, ABS>(p, zl, ZL, Lg, wc, ma);
+      // weights are only needed in full when traced or final
+      const bool early = BG != 0 && !p.trace && !last && p.z % 32 == 0;
+      local_check<BG, MAXW, LANES, ABS>(p, zl, ZL, Lg, wc, ma, early, lane_valid[0] && !gs.done[0],
+                                        lane_valid[1] && !gs.done[1]);
       if (active) {
 #pragma unroll
         for (int l = 0; l < LANES; ++l) {
