@@ -119,6 +119,30 @@ def test_ragged_batches(cuda_ok, batch):
         _oracle_cmp(bg, bg.m_bg, nr.DecodeConfig(max_iter=8), blocks)
 
 
+@pytest.mark.parametrize("bg_id,z,early", [("BG1", 384, "none"), ("BG2", 384, "syndrome"),
+                                           ("BG1", 288, "syndrome"), ("BG2", 52, "none")])
+def test_large_batch_position_invariance(cuda_ok, bg_id, z, early):
+    """A batch of many waves (ragged count): every codeword's result is
+    independent of where it sits in the batch and of its lane partner. A
+    block of distinct codewords is tiled with a shift so each one lands in
+    both lanes of a pair and in the first and last waves; the first tile is
+    pinned against the oracle."""
+    bg = nr.load_basegraph(bg_id, z)
+    cfg = nr.DecodeConfig(max_iter=6, early_stop=early)
+    _, llr = noisy_llrs(bg, bg.m_bg, 1.0, 37, seed=(z, 99))
+    base = oracle.quantize_i8(llr, z)
+    reps = 4111 // len(base) + 1
+    tiled = np.concatenate([np.roll(base, i, axis=0) for i in range(reps)])[:4111]
+    res = nr.decode(tiled, bg, cfg)
+    ref = oracle.decode(base, bg, cfg)
+    for i in range(reps):
+        lo, hi = i * len(base), min((i + 1) * len(base), len(tiled))
+        idx = (np.arange(lo, hi) - lo - i) % len(base)       # row of base at each position
+        assert np.array_equal(res.bits[lo:hi], ref["bits"][idx]), i
+        assert np.array_equal(res.iterations[lo:hi], ref["iterations"][idx]), i
+        assert np.array_equal(res.syndrome_weight[lo:hi], ref["syndrome_weight"][idx]), i
+
+
 def test_empty_batch(cuda_ok):
     bg = nr.load_basegraph("BG2", 16)
     res = nr.decode(np.zeros((0, 832), np.int8), bg, nr.DecodeConfig())
