@@ -149,9 +149,11 @@ def test_empty_batch(cuda_ok):
     assert res.bits.shape == (0, 160) and res.iterations.shape == (0,)
 
 
-@pytest.mark.parametrize("rows", [4, 5, 17, 30, 45])
+@pytest.mark.parametrize("rows", [4, 5, 6, 7, 8, 17, 23, 30, 45])
 def test_partial_rows_vs_oracle(cuda_ok, rows):
-    for bg_id, z in (("BG1", 384), ("BG2", 44)):
+    # BG1 Z=384 / 288: register-row kernels (rows 0..min(rows,6)-1 from
+    # registers, the rest as units, a pair cut in half at odd rows_used)
+    for bg_id, z in (("BG1", 384), ("BG1", 288), ("BG2", 44)):
         bg = nr.load_basegraph(bg_id, z)
         if rows > bg.m_bg:
             continue
