@@ -12,7 +12,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import paper_2009_05534_b200 as nr
-from paper_2009_05534_b200.shard import decode_sharded, merge_results, shard_bounds
+from paper_2009_05534_b200.shard import (assign_groups, decode_mixed_sharded, decode_sharded, group_cost,
+                                         merge_results, shard_bounds)
 from paper_2009_05534_b200.synth import noisy_llrs
 from oracle import oracle
 
@@ -71,3 +72,41 @@ def test_merge_results_keeps_order():
     b = nr.DecodeResult(np.ones((1, 3), np.uint8), np.array([3]), np.array([True]), np.array([0]))
     m = merge_results([a, b])
     assert m.iterations.tolist() == [1, 2, 3] and m.bits.shape == (3, 3) and m.crc_ok is None
+
+
+def test_assign_groups_balances_longest_first():
+    costs = [9.0, 7.0, 6.0, 5.0, 4.0, 3.0, 2.0, 1.0]
+    owner = assign_groups(costs, 3)
+    loads = [sum(c for c, o in zip(costs, owner) if o == r) for r in range(3)]
+    assert max(loads) - min(loads) <= 2.0 and sorted(set(owner)) == [0, 1, 2]
+    assert assign_groups(costs, 1) == [0] * len(costs)
+    assert assign_groups(costs, 3) == owner                      # deterministic
+
+
+def _mixed_worker(rank, world, port, shapes, blocks, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    groups = [(nr.load_basegraph(b, z), rows) for b, z, rows in shapes]
+    res = decode_mixed_sharded(groups, blocks, nr.DecodeConfig(max_iter=6), decode_fn=_oracle_decode)
+    if rank == 0:
+        np.savez(out_path, **{f"b{i}": r.bits for i, r in enumerate(res)},
+                 **{f"i{i}": r.iterations for i, r in enumerate(res)})
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_mixed_groups_match_single_process(tmp_path):
+    shapes = [("BG1", 16, 46), ("BG2", 7, 42), ("BG1", 12, 8), ("BG2", 30, 20), ("BG2", 2, 42)]
+    blocks = []
+    for b, z, rows in shapes:
+        bg = nr.load_basegraph(b, z)
+        _, llr = noisy_llrs(bg, rows, 1.5, 5, seed=(z, rows))
+        blocks.append(oracle.quantize_i8(llr, z))
+    costs = [group_cost(nr.load_basegraph(b, z), rows, 5, 6) for b, z, rows in shapes]
+    assert len(set(assign_groups(costs, 2))) == 2                # both ranks get work
+    out = tmp_path / "mixed.npz"
+    mp.spawn(_mixed_worker, args=(2, _free_port(), shapes, blocks, str(out)), nprocs=2, join=True)
+    got = np.load(out)
+    for i, (b, z, rows) in enumerate(shapes):
+        ref = oracle.decode(blocks[i], nr.load_basegraph(b, z), nr.DecodeConfig(max_iter=6), threads=1)
+        assert np.array_equal(got[f"b{i}"], ref["bits"]) and np.array_equal(got[f"i{i}"], ref["iterations"])
