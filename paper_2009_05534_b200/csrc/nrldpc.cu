@@ -67,6 +67,7 @@ struct CtaState {
 
 constexpr int kLutBytes = 256;
 constexpr int kCtaBytes = 32;
+static_assert(sizeof(CtaState) == kCtaBytes, "CtaState layout");
 
 // k_decode_i8's shared layout: LUT, CTA state, group states, then per group
 // L and messages from this 16-aligned offset
@@ -1189,7 +1190,7 @@ void find_beta_arith(double beta, KParams* kp) {
 Shape choose_shape_float(const nrldpc_plan* p) {
   const size_t smem_max = 232448;
   const size_t lb = align16((size_t)p->n_blocks * p->z * 4);
-  auto smem_f = [&](int g) { return (size_t)16 + 16 + sizeof(FltState) * g + g * lb; };
+  auto smem_f = [&](int g) { return (size_t)kCtaBytes + 16 + sizeof(FltState) * g + g * lb; };
   int best_g = 1;
   double best_waste = 1e9;
   for (int g = 1; g * p->z <= 512; ++g) {

@@ -84,8 +84,8 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
   constexpr int LANES = F::lanes;
   extern __shared__ __align__(16) uint8_t smem[];
   CtaState* cta = reinterpret_cast<CtaState*>(smem);
-  FltState* gstate = reinterpret_cast<FltState*>(smem + 16);
-  const uint32_t data_off = (16u + (uint32_t)sizeof(FltState) * p.groups + 15u) & ~15u;
+  FltState* gstate = reinterpret_cast<FltState*>(smem + kCtaBytes);
+  const uint32_t data_off = ((uint32_t)kCtaBytes + (uint32_t)sizeof(FltState) * p.groups + 15u) & ~15u;
 
   const int tid = threadIdx.x;
   const bool st_ok = tid < p.groups * p.z;
