@@ -749,7 +749,9 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
   const uint32_t data_off = data_offset(p.groups);
 
   const int tid = threadIdx.x;
-  const bool st_ok = tid < p.groups * p.z;           // not a padding thread
+  // not a padding thread; register-row shapes have one group of Z threads
+  // with Z in {288, 320, 352, 384}, a whole number of warps (host-checked)
+  const bool st_ok = NREG > 0 || tid < p.groups * p.z;
   const int g = st_ok ? tid / p.z : p.groups - 1;
   const int z = st_ok ? tid - g * p.z : (tid - g * p.z) % p.z;
   const long long cw0 = ((long long)blockIdx.x * p.groups + g) * LANES;
@@ -1309,10 +1311,10 @@ Shape choose_shape(const nrldpc_plan* p, int max_lanes) {
     // of rows 0..5 in registers whenever those rows exist (fewer shared
     // accesses, and one kernel for all large Z, which matters when many Z
     // decode concurrently). Rows 0..1 / 0..3 when rows_used < 6.
-    const bool big = p->schedule == 1 && p->z > 256 && p->z <= 384;
+    const bool big = p->schedule == 1 && p->z > 256 && p->z <= 384 && p->z % 32 == 0;
     if (fits && !big) {
       lanes = 2;
-    } else if (p->schedule == 1 && p->z <= 384) {
+    } else if (p->schedule == 1 && p->z <= 384 && p->z % 32 == 0) {
       for (int nr : {6, 4, 2}) {
         if (nr > p->rows) continue;
         if (smem_for(1, align16(n_pos * 2), msg_bytes(2, RowW<1>::e0[nr])) <= smem_max) {
