@@ -600,18 +600,20 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
     // precomputed byte offsets; each unit's descriptor is loaded one unit
     // ahead so the dispatch after a barrier does not wait on the constant
     // cache.
-    uint4 na = p.unit_a[0];
+    uint32_t ncode = p.unit_a[0].x;
     // The barrier that closes a layer runs inside the next unit, after its
     // thread-private prologue (tables, addresses, own messages) and before
     // its first posterior load, so warps arriving early do useful work.
 #pragma unroll 1
     for (int u = 0; u < p.n_units; ++u) {
-      // only the dispatch word set is prefetched (fewer loop-carried copies);
-      // the second half is needed later in the body
-      const uint4 A = na;
+      // only the dispatch code is prefetched (one loop-carried copy); the
+      // offsets are needed inside the body, where their load overlaps the
+      // dispatch
+      const uint32_t code = ncode;
+      const uint4 A = p.unit_a[u];
       const uint4 B = p.unit_b[u];
-      na = p.unit_a[u + 1];
-      dispatch_unit<BG, NREG>(A.x, [&](auto WA, auto WB) {
+      ncode = p.unit_a[u + 1].x;
+      dispatch_unit<BG, NREG>(code, [&](auto WA, auto WB) {
         constexpr int wa = decltype(WA)::value, wb = decltype(WB)::value;
         if constexpr (wb == 0)
           process_row<wa, LANES, false, ABS, false>(p, A.z, A.w, wa, c.zl, c.ZL, c.Lg, c.Mz, c.Ms, rm.r4, c.lut, c.k,
