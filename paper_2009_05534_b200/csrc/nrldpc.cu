@@ -493,24 +493,39 @@ __device__ __forceinline__ void dispatch_w(int w, F&& f) {
 // unit occurs per iteration of the full graph.
 // NREG: rows 0..NREG-1 run from registers, so their weights (19 for the four
 // core rows, 3 for row 4) never reach the unit loop and get no body.
+__device__ __forceinline__ bool wge(int w, int k) {
+  int r;
+  asm("{ .reg .pred q; setp.ge.s32 q, %1, %2; selp.s32 %0, 1, 0, q; }" : "=r"(r) : "r"(w), "r"(k));
+  return r != 0;
+}
+
 template <int BG, int NREG, typename F>
 __device__ __forceinline__ void dispatch_unit(uint32_t code, F&& f) {
   const int c = (int)code;
+  // pairs (code >= 256) and single rows get separate chains
 #define NR_U(a, b) else if (weq(c, (a) | ((b) << 8))) f(IC<a>{}, IC<b>{})
   if constexpr (BG == 1) {
-    if (false) {}
-    NR_U(5, 5); NR_U(5, 4); NR_U(7, 0); NR_U(6, 6); NR_U(6, 0); NR_U(4, 5); NR_U(9, 0); NR_U(6, 5);
-    NR_U(10, 0); NR_U(8, 0); NR_U(5, 0); NR_U(4, 0);
-    if constexpr (NREG < 4) {
-      if (weq(c, 19)) f(IC<19>{}, IC<0>{});
-    }
-    if constexpr (NREG < 6) {
-      if (weq(c, 3)) f(IC<3>{}, IC<0>{});
+    if (wge(c, 256)) {
+      if (false) {}
+      NR_U(5, 5); NR_U(5, 4); NR_U(6, 6); NR_U(4, 5); NR_U(6, 5);
+    } else {
+      if (false) {}
+      NR_U(7, 0); NR_U(6, 0); NR_U(9, 0); NR_U(10, 0); NR_U(8, 0); NR_U(5, 0); NR_U(4, 0);
+      else if constexpr (NREG < 6) {
+        if (weq(c, 3)) f(IC<3>{}, IC<0>{});
+        else if constexpr (NREG < 4) {
+          if (weq(c, 19)) f(IC<19>{}, IC<0>{});
+        }
+      }
     }
   } else {
-    if (false) {}
-    NR_U(4, 4); NR_U(4, 0); NR_U(5, 0); NR_U(4, 3); NR_U(6, 0); NR_U(5, 4); NR_U(5, 3); NR_U(8, 0);
-    NR_U(10, 0); NR_U(3, 4); NR_U(3, 0);
+    if (wge(c, 256)) {
+      if (false) {}
+      NR_U(4, 4); NR_U(4, 3); NR_U(5, 4); NR_U(5, 3); NR_U(3, 4);
+    } else {
+      if (false) {}
+      NR_U(4, 0); NR_U(5, 0); NR_U(6, 0); NR_U(8, 0); NR_U(10, 0); NR_U(3, 0);
+    }
   }
 #undef NR_U
 }
