@@ -565,19 +565,6 @@ struct RegMsg {
         }
     }
   }
-  __device__ __forceinline__ void rotate() {
-    if constexpr (nq > 1) {
-      uint32_t h[10];
-#pragma unroll
-      for (int i = 0; i < 10; ++i) h[i] = q[0][i];
-#pragma unroll
-      for (int k = 0; k + 1 < nq; ++k)
-#pragma unroll
-        for (int i = 0; i < 10; ++i) q[k][i] = q[k + 1][i];
-#pragma unroll
-      for (int i = 0; i < 10; ++i) q[nq - 1][i] = h[i];
-    }
-  }
 };
 
 template <int BG, int MAXW, int LANES, int NREG, bool ABS>
