@@ -256,7 +256,7 @@ def unpack_bits(words: np.ndarray, k: int) -> np.ndarray:
     """(B, ceil(K/32)) LSB-first uint32 words -> (B, K) uint8 0/1."""
     w = np.ascontiguousarray(words).view(np.uint32).astype("<u4", copy=False)
     bits = np.unpackbits(w.view(np.uint8).reshape(w.shape[0], -1), axis=1, bitorder="little")
-    return bits[:, :k]
+    return bits if bits.shape[1] == k else np.ascontiguousarray(bits[:, :k])
 
 
 def _rows_used(n_c: int, bg) -> int:
@@ -288,16 +288,41 @@ def decode(llrs, bg, cfg: DecodeConfig, trace: list | None = None) -> DecodeResu
         raise ValueError("packed int8 decode needs a multiple of 4 codewords")
     rows_used = _rows_used(arr.shape[-1], bg)
     if cfg.precision is Precision.INT8:
-        wide = arr.astype(np.int32)  # decoder.py:286 (astype semantics)
-        if wide.size and np.abs(wide).max() > INT8_SAT:
-            raise ValueError("int8 LLR magnitudes must be at most 127")
-        host = np.ascontiguousarray(wide.astype(np.int8))
+        if arr.dtype == np.int8:
+            # the only out-of-range int8 value is -128; the decode kernel
+            # flags it and the call raises the same ValueError (no result)
+            host = np.ascontiguousarray(arr)
+        else:
+            wide = arr.astype(np.int32)  # decoder.py:286 (astype semantics)
+            if wide.size and np.abs(wide).max() > INT8_SAT:
+                raise ValueError("int8 LLR magnitudes must be at most 127")
+            host = np.ascontiguousarray(wide.astype(np.int8))
     else:
         host = np.ascontiguousarray(arr.astype(_FLOAT_DTYPE[cfg.precision]))
-    import torch
     plan = get_plan(bg, rows_used, cfg)
+    if trace is None:
+        # host buffers straight through the C ABI's pipelined path (chunked
+        # H2D copies overlapped with the decode, one result copy-out)
+        batch = int(host.shape[0])
+        if batch == 0:
+            return _empty_result(plan.k, cfg)
+        out = plan.decode_host(host, chunks=max(1, min(12, batch // 86)))
+        return DecodeResult(
+            bits=unpack_bits(out["bits"], plan.k),
+            iterations=out["iters"].astype(np.int64),
+            success=out["success"].astype(bool),
+            syndrome_weight=out["synd"].astype(np.int64),
+            crc_ok=out["crc_ok"].astype(bool) if cfg.early_stop is EarlyStop.CRC else None,
+        )
+    import torch
     dev_in = torch.from_numpy(host).to(f"cuda:{plan.device}", non_blocking=False)
     return _run(plan, dev_in, cfg, trace)
+
+
+def _empty_result(k: int, cfg: DecodeConfig) -> DecodeResult:
+    return DecodeResult(bits=np.zeros((0, k), np.uint8), iterations=np.zeros(0, np.int64),
+                        success=np.zeros(0, bool), syndrome_weight=np.zeros(0, np.int64),
+                        crc_ok=np.zeros(0, bool) if cfg.early_stop is EarlyStop.CRC else None)
 
 
 def _decode_torch(llrs, bg, cfg, trace):
@@ -324,9 +349,7 @@ def _run(plan: Plan, dev_in, cfg: DecodeConfig, trace, flooding: bool = False) -
     batch = int(dev_in.shape[0])
     k = plan.k
     if batch == 0:
-        return DecodeResult(bits=np.zeros((0, k), np.uint8), iterations=np.zeros(0, np.int64),
-                            success=np.zeros(0, bool), syndrome_weight=np.zeros(0, np.int64),
-                            crc_ok=np.zeros(0, bool) if cfg.early_stop is EarlyStop.CRC else None)
+        return _empty_result(k, cfg)
     out = plan.alloc_outputs(batch, trace=trace is not None)
     if flooding:
         plan.decode_flooding_device(dev_in, out)

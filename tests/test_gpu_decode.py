@@ -228,6 +228,21 @@ def test_out_of_range_device_input_raises(cuda_ok):
         nr.decode(x, bg, nr.DecodeConfig())
 
 
+@pytest.mark.parametrize("bg_id,z,batch", [("BG2", 16, 3), ("BG1", 384, 40), ("BG1", 13, 1)])
+def test_out_of_range_host_int8_raises_and_plan_stays_usable(cuda_ok, bg_id, z, batch):
+    """Host int8 input goes straight to the device; a -128 anywhere (vector or
+    scalar prologue) raises the reference's ValueError, and the next call on
+    the same plan decodes normally."""
+    bg = nr.load_basegraph(bg_id, z)
+    _, llr = noisy_llrs(bg, bg.m_bg, 2.0, batch, seed=(z, 5))
+    blocks = oracle.quantize_i8(llr, z)
+    bad = blocks.copy()
+    bad[-1, -3] = -128
+    with pytest.raises(ValueError, match="at most 127"):
+        nr.decode(bad, bg, nr.DecodeConfig(max_iter=4))
+    _oracle_cmp(bg, bg.m_bg, nr.DecodeConfig(max_iter=4), blocks)
+
+
 def test_native_library_is_the_compute_path(cuda_ok):
     bg = nr.load_basegraph("BG2", 64)
     nr.decode(np.zeros((4, 3328), np.int8), bg, nr.DecodeConfig(max_iter=2))
