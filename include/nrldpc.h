@@ -151,6 +151,21 @@ int nrldpc_decode_host(nrldpc_plan* plan, const void* llr_host, int64_t batch,
                        uint8_t* success, uint8_t* crc_ok, int chunks);
 
 /*
+ * The same call split in two for pipelined serving: _async enqueues the
+ * copies and the decode and returns a ticket at once; nrldpc_host_wait
+ * blocks until that call's results are in the host buffers (and reports its
+ * status). The plan keeps two calls in flight, so a caller that waits for
+ * call i after issuing call i+1 overlaps i+1's input copies with i's decode.
+ * Issuing a third call first retires the oldest one. Host buffers must stay
+ * valid until the wait returns; use pinned memory for overlap.
+ */
+int nrldpc_decode_host_async(nrldpc_plan* plan, const void* llr_host, int64_t batch,
+                             uint32_t* bits, int32_t* iters, int32_t* synd,
+                             uint8_t* success, uint8_t* crc_ok, int chunks,
+                             int64_t* ticket);
+int nrldpc_host_wait(nrldpc_plan* plan, int64_t ticket);
+
+/*
  * Synthetic traffic on the GPU. nrldpc_encode: systematic
  * encoding (codec.py:66-139), msgs (batch, K) bytes 0/1 -> codewords
  * (batch, n_c) bytes 0/1, bit-exact. nrldpc_channel_awgn: BPSK + AWGN

@@ -33,6 +33,8 @@ EXPORTS = (
     "nrldpc_demap_quantize",
     "nrldpc_decode",
     "nrldpc_decode_host",
+    "nrldpc_decode_host_async",
+    "nrldpc_host_wait",
     "nrldpc_decode_flooding",
     "nrldpc_encode",
     "nrldpc_channel_awgn",
@@ -84,6 +86,10 @@ def load() -> ctypes.CDLL:
     lib.nrldpc_decode.restype = c_int
     lib.nrldpc_decode_host.argtypes = [c_void_p, c_void_p, c_int64] + [c_void_p] * 5 + [c_int]
     lib.nrldpc_decode_host.restype = c_int
+    lib.nrldpc_decode_host_async.argtypes = [c_void_p, c_void_p, c_int64] + [c_void_p] * 5 + [c_int, c_void_p]
+    lib.nrldpc_decode_host_async.restype = c_int
+    lib.nrldpc_host_wait.argtypes = [c_void_p, c_int64]
+    lib.nrldpc_host_wait.restype = c_int
     lib.nrldpc_decode_flooding.argtypes = [c_void_p, c_void_p, c_int64] + [c_void_p] * 8
     lib.nrldpc_decode_flooding.restype = c_int
     lib.nrldpc_encode.argtypes = [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]

@@ -1061,15 +1061,24 @@ struct nrldpc_plan {
   int schedule = 0;  // 0 generic, 1/2: compile-time BG1/BG2 row schedule
   KParams base{};    // graph tables + config, before the shape-dependent scaling
   Shape main;        // the launch shape
-  // host-path staging (nrldpc_decode_host)
+  // host-path staging (nrldpc_decode_host[_async])
   std::mutex host_mu;
-  // host pipeline: streams[0] copies in (in chunk order) and out; the rest
-  // decode chunks as their input lands (one event per chunk)
-  static constexpr int kHostStreams = 17;
+  // host pipeline: streams[0] copies inputs in (in chunk order), streams[1]
+  // copies results out, the rest decode chunks as their input lands (one
+  // event per chunk). Two slots of device buffers let one call's copies and
+  // decode overlap the next call's (nrldpc_decode_host_async).
+  static constexpr int kHostStreams = 18;
+  static constexpr int kSlots = 2;
   cudaStream_t streams[kHostStreams] = {};
   std::vector<cudaEvent_t> chunk_ev;
-  void* d_buf = nullptr;
-  size_t d_cap = 0;
+  struct Slot {
+    void* d_buf = nullptr;
+    size_t d_cap = 0;
+    int32_t* h_status = nullptr;  // pinned: the slot's status word lands here
+    cudaEvent_t done = nullptr;   // recorded after the slot's result copies
+    int64_t ticket = -1;          // call in flight in this slot (-1: none)
+  } slot[kSlots];
+  int64_t next_ticket = 0;
 };
 
 namespace {
@@ -1871,7 +1880,11 @@ int nrldpc_plan_destroy(nrldpc_plan* plan) {
   for (auto& s : plan->streams)
     if (s) cudaStreamDestroy(s);
   for (auto& e : plan->chunk_ev) cudaEventDestroy(e);
-  if (plan->d_buf) cudaFree(plan->d_buf);
+  for (auto& sl : plan->slot) {
+    if (sl.done) cudaEventSynchronize(sl.done), cudaEventDestroy(sl.done);
+    if (sl.d_buf) cudaFree(sl.d_buf);
+    if (sl.h_status) cudaFreeHost(sl.h_status);
+  }
   if (plan->d_crc_tab) cudaFree(plan->d_crc_tab);
   cudaSetDevice(prev);
   delete plan;
@@ -1977,35 +1990,31 @@ int nrldpc_decode(nrldpc_plan* plan, const void* llr, int64_t batch, uint32_t* b
   return decode_impl(plan, llr, batch, o, (cudaStream_t)stream);
 }
 
-int nrldpc_decode_host(nrldpc_plan* plan, const void* llr_host, int64_t batch, uint32_t* bits,
-                       int32_t* iters, int32_t* synd, uint8_t* success, uint8_t* crc_ok, int chunks) {
-  g_launches = 0;
-  if (!plan) return fail(NRLDPC_EINVAL, "plan is NULL");
-  if (batch < 0) return fail(NRLDPC_EINVAL, "batch must be non-negative");
-  if (batch == 0) return NRLDPC_OK;
-  if (!llr_host || !bits || !iters || !synd || !success) return fail(NRLDPC_EINVAL, "NULL buffer");
-  if (plan->early_stop == NRLDPC_STOP_CRC && !crc_ok)
-    return fail(NRLDPC_EINVAL, "crc mode needs a crc_ok buffer");
-  std::lock_guard<std::mutex> lock(plan->host_mu);
-  NR_CUDA(cudaSetDevice(plan->device));
+// Enqueue one host-buffer decode into slot `si` (caller holds host_mu and has
+// retired the slot's previous call). Returns the number of decode launches
+// through *launches.
+static int host_enqueue(nrldpc_plan* plan, int si, const void* llr_host, int64_t batch, uint32_t* bits,
+                        int32_t* iters, int32_t* synd, uint8_t* success, uint8_t* crc_ok, int chunks,
+                        int* launches_out) {
+  auto& sl = plan->slot[si];
   const size_t esz = plan->precision == NRLDPC_INT8 ? 1 : (plan->precision == NRLDPC_F16 ? 2 : 4);
   const size_t n_c = (size_t)plan->n_blocks * plan->z;
   const size_t words = plan->base.words;
   const size_t per_cw_in = n_c * esz;
-  const size_t per_cw_out = words * 4 + 4 + 4 + 1 + 1;
   const size_t need = align16(batch * per_cw_in) + align16(batch * words * 4) + align16(batch * 4) * 2 +
                       align16(batch) * 2 + 16;
-  if (need > plan->d_cap) {
-    if (plan->d_buf) cudaFree(plan->d_buf);
-    plan->d_buf = nullptr;
-    plan->d_cap = 0;
-    NR_CUDA(cudaMalloc(&plan->d_buf, need));
-    plan->d_cap = need;
+  if (need > sl.d_cap) {
+    if (sl.d_buf) cudaFree(sl.d_buf);
+    sl.d_buf = nullptr;
+    sl.d_cap = 0;
+    NR_CUDA(cudaMalloc(&sl.d_buf, need));
+    sl.d_cap = need;
   }
-  (void)per_cw_out;
+  if (!sl.h_status) NR_CUDA(cudaMallocHost(reinterpret_cast<void**>(&sl.h_status), sizeof(int32_t)));
+  if (!sl.done) NR_CUDA(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
   for (auto& s : plan->streams)
     if (!s) NR_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  uint8_t* base = static_cast<uint8_t*>(plan->d_buf);
+  uint8_t* base = static_cast<uint8_t*>(sl.d_buf);
   uint8_t* d_llr = base;
   uint32_t* d_bits = reinterpret_cast<uint32_t*>(base + align16(batch * per_cw_in));
   int32_t* d_iters = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(d_bits) + align16(batch * words * 4));
@@ -2013,20 +2022,14 @@ int nrldpc_decode_host(nrldpc_plan* plan, const void* llr_host, int64_t batch, u
   uint8_t* d_succ = reinterpret_cast<uint8_t*>(d_synd) + align16(batch * 4);
   uint8_t* d_crc = d_succ + align16(batch);
   int32_t* d_status = reinterpret_cast<int32_t*>(d_crc + align16(batch));
-  // Pipeline: the copy stream moves the chunks in order at full link rate,
-  // each chunk's decode waits only for its own input, and many chunk kernels
-  // are in flight at once so their partial waves pack the SMs. Results come
-  // back in one pass at the end (they are ~4% of the input bytes).
-  cudaStream_t cp = plan->streams[0];
-  constexpr int n_comp = nrldpc_plan::kHostStreams - 1;
-  static const bool dbg = getenv("NRLDPC_HOST_TIMING") != nullptr;
-  cudaEvent_t t0 = nullptr, t1 = nullptr;
-  if (dbg) {
-    cudaEventCreate(&t0);
-    cudaEventCreate(&t1);
-    cudaEventRecord(t0, cp);
-  }
-  NR_CUDA(cudaMemsetAsync(d_status, 0, 4, cp));
+  // Pipeline: the copy-in stream moves the chunks in order at full link
+  // rate, each chunk's decode waits only for its own input, and many chunk
+  // kernels are in flight at once so their partial waves pack the SMs.
+  // Results come back in one pass on the copy-out stream (they are ~4% of
+  // the input bytes), so the next call's inputs never queue behind them.
+  cudaStream_t cin = plan->streams[0], cout = plan->streams[1];
+  constexpr int n_comp = nrldpc_plan::kHostStreams - 2;
+  NR_CUDA(cudaMemsetAsync(d_status, 0, 4, cin));
   if (chunks < 1) chunks = 1;
   const int64_t per_lane_cta = (int64_t)plan->main.groups * plan->main.lanes;
   int64_t chunk = (batch + chunks - 1) / chunks;
@@ -2042,9 +2045,9 @@ int nrldpc_decode_host(nrldpc_plan* plan, const void* llr_host, int64_t batch, u
     const int64_t b0 = idx * chunk;
     const int64_t nb = std::min<int64_t>(chunk, batch - b0);
     NR_CUDA(cudaMemcpyAsync(d_llr + b0 * per_cw_in, static_cast<const uint8_t*>(llr_host) + b0 * per_cw_in,
-                            nb * per_cw_in, cudaMemcpyHostToDevice, cp));
-    NR_CUDA(cudaEventRecord(plan->chunk_ev[idx], cp));
-    cudaStream_t st = plan->streams[1 + idx % n_comp];
+                            nb * per_cw_in, cudaMemcpyHostToDevice, cin));
+    NR_CUDA(cudaEventRecord(plan->chunk_ev[idx], cin));
+    cudaStream_t st = plan->streams[2 + idx % n_comp];
     NR_CUDA(cudaStreamWaitEvent(st, plan->chunk_ev[idx], 0));
     KOut o{d_bits + b0 * words, d_iters + b0, d_synd + b0, d_succ + b0,
            crc_ok ? d_crc + b0 : nullptr, nullptr, nullptr, d_status};
@@ -2054,28 +2057,112 @@ int nrldpc_decode_host(nrldpc_plan* plan, const void* llr_host, int64_t batch, u
     launches += g_launches;
   }
   for (int c = 0; c < n_comp; ++c) {
-    NR_CUDA(cudaEventRecord(plan->chunk_ev[n_chunks + c], plan->streams[1 + c]));
-    NR_CUDA(cudaStreamWaitEvent(cp, plan->chunk_ev[n_chunks + c], 0));
+    NR_CUDA(cudaEventRecord(plan->chunk_ev[n_chunks + c], plan->streams[2 + c]));
+    NR_CUDA(cudaStreamWaitEvent(cout, plan->chunk_ev[n_chunks + c], 0));
   }
-  NR_CUDA(cudaMemcpyAsync(bits, d_bits, batch * words * 4, cudaMemcpyDeviceToHost, cp));
-  NR_CUDA(cudaMemcpyAsync(iters, d_iters, batch * 4, cudaMemcpyDeviceToHost, cp));
-  NR_CUDA(cudaMemcpyAsync(synd, d_synd, batch * 4, cudaMemcpyDeviceToHost, cp));
-  NR_CUDA(cudaMemcpyAsync(success, d_succ, batch, cudaMemcpyDeviceToHost, cp));
-  if (crc_ok) NR_CUDA(cudaMemcpyAsync(crc_ok, d_crc, batch, cudaMemcpyDeviceToHost, cp));
-  int32_t status = 0;
-  NR_CUDA(cudaMemcpyAsync(&status, d_status, 4, cudaMemcpyDeviceToHost, cp));
-  if (dbg) cudaEventRecord(t1, cp);
-  NR_CUDA(cudaStreamSynchronize(cp));
+  NR_CUDA(cudaMemcpyAsync(bits, d_bits, batch * words * 4, cudaMemcpyDeviceToHost, cout));
+  NR_CUDA(cudaMemcpyAsync(iters, d_iters, batch * 4, cudaMemcpyDeviceToHost, cout));
+  NR_CUDA(cudaMemcpyAsync(synd, d_synd, batch * 4, cudaMemcpyDeviceToHost, cout));
+  NR_CUDA(cudaMemcpyAsync(success, d_succ, batch, cudaMemcpyDeviceToHost, cout));
+  if (crc_ok) NR_CUDA(cudaMemcpyAsync(crc_ok, d_crc, batch, cudaMemcpyDeviceToHost, cout));
+  NR_CUDA(cudaMemcpyAsync(sl.h_status, d_status, 4, cudaMemcpyDeviceToHost, cout));
+  NR_CUDA(cudaEventRecord(sl.done, cout));
+  *launches_out = launches;
+  return NRLDPC_OK;
+}
+
+// Retire the call in slot `si`: wait for its results and report its status.
+static int host_retire(nrldpc_plan* plan, int si) {
+  auto& sl = plan->slot[si];
+  if (sl.ticket < 0) return NRLDPC_OK;
+  sl.ticket = -1;
+  NR_CUDA(cudaEventSynchronize(sl.done));
+  if (*sl.h_status) return fail(NRLDPC_EINVAL, "int8 LLR magnitudes must be at most 127");
+  return NRLDPC_OK;
+}
+
+static int host_check_args(const nrldpc_plan* plan, int64_t batch, const void* llr_host, const void* bits,
+                           const void* iters, const void* synd, const void* success, const void* crc_ok) {
+  if (!plan) return fail(NRLDPC_EINVAL, "plan is NULL");
+  if (batch < 0) return fail(NRLDPC_EINVAL, "batch must be non-negative");
+  if (batch == 0) return NRLDPC_OK;
+  if (!llr_host || !bits || !iters || !synd || !success) return fail(NRLDPC_EINVAL, "NULL buffer");
+  if (plan->early_stop == NRLDPC_STOP_CRC && !crc_ok)
+    return fail(NRLDPC_EINVAL, "crc mode needs a crc_ok buffer");
+  return NRLDPC_OK;
+}
+
+int nrldpc_decode_host(nrldpc_plan* plan, const void* llr_host, int64_t batch, uint32_t* bits,
+                       int32_t* iters, int32_t* synd, uint8_t* success, uint8_t* crc_ok, int chunks) {
+  g_launches = 0;
+  int rc = host_check_args(plan, batch, llr_host, bits, iters, synd, success, crc_ok);
+  if (rc != NRLDPC_OK || batch == 0) return rc;
+  std::lock_guard<std::mutex> lock(plan->host_mu);
+  NR_CUDA(cudaSetDevice(plan->device));
+  // a synchronous call retires whatever is still in flight first
+  for (int i = 0; i < nrldpc_plan::kSlots; ++i) {
+    rc = host_retire(plan, i);
+    if (rc != NRLDPC_OK) return rc;
+  }
+  static const bool dbg = getenv("NRLDPC_HOST_TIMING") != nullptr;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  if (dbg) {
+    cudaEventCreate(&t0);
+    cudaEventCreate(&t1);
+    cudaEventRecord(t0, plan->streams[0] ? plan->streams[0] : nullptr);
+  }
+  int launches = 0;
+  rc = host_enqueue(plan, 0, llr_host, batch, bits, iters, synd, success, crc_ok, chunks, &launches);
+  if (rc != NRLDPC_OK) return rc;
+  plan->slot[0].ticket = plan->next_ticket++;
+  if (dbg) cudaEventRecord(t1, plan->streams[1]);
+  rc = host_retire(plan, 0);
   if (dbg) {
     float ms = 0;
+    cudaEventSynchronize(t1);
     cudaEventElapsedTime(&ms, t0, t1);
     fprintf(stderr, "decode_host gpu span %.3f ms\n", ms);
     cudaEventDestroy(t0);
     cudaEventDestroy(t1);
   }
   g_launches = launches;
-  if (status) return fail(NRLDPC_EINVAL, "int8 LLR magnitudes must be at most 127");
+  return rc;
+}
+
+int nrldpc_decode_host_async(nrldpc_plan* plan, const void* llr_host, int64_t batch, uint32_t* bits,
+                             int32_t* iters, int32_t* synd, uint8_t* success, uint8_t* crc_ok, int chunks,
+                             int64_t* ticket) {
+  g_launches = 0;
+  if (!ticket) return fail(NRLDPC_EINVAL, "NULL ticket");
+  *ticket = -1;
+  int rc = host_check_args(plan, batch, llr_host, bits, iters, synd, success, crc_ok);
+  if (rc != NRLDPC_OK) return rc;
+  std::lock_guard<std::mutex> lock(plan->host_mu);
+  NR_CUDA(cudaSetDevice(plan->device));
+  const int64_t t = plan->next_ticket++;
+  if (batch == 0) {
+    *ticket = t;
+    return NRLDPC_OK;
+  }
+  const int si = (int)(t % nrldpc_plan::kSlots);
+  rc = host_retire(plan, si);  // the slot's previous call (its caller may still wait: already done)
+  if (rc != NRLDPC_OK) return rc;
+  int launches = 0;
+  rc = host_enqueue(plan, si, llr_host, batch, bits, iters, synd, success, crc_ok, chunks, &launches);
+  if (rc != NRLDPC_OK) return rc;
+  plan->slot[si].ticket = t;
+  *ticket = t;
+  g_launches = launches;
   return NRLDPC_OK;
+}
+
+int nrldpc_host_wait(nrldpc_plan* plan, int64_t ticket) {
+  if (!plan) return fail(NRLDPC_EINVAL, "plan is NULL");
+  std::lock_guard<std::mutex> lock(plan->host_mu);
+  NR_CUDA(cudaSetDevice(plan->device));
+  for (int i = 0; i < nrldpc_plan::kSlots; ++i)
+    if (plan->slot[i].ticket == ticket) return host_retire(plan, i);
+  return NRLDPC_OK;  // already retired (or an empty batch)
 }
 
 }  // extern "C"

@@ -209,6 +209,25 @@ class Plan:
             out[k] = t.numpy().view(d)
         return out
 
+    def decode_host_async(self, llr: np.ndarray, chunks: int = 12, out: dict | None = None) -> tuple[int, dict]:
+        """Enqueue a host-buffer decode (nrldpc_decode_host_async); returns
+        (ticket, out). ``llr`` and ``out`` must stay alive (and should be
+        pinned) until ``host_wait(ticket)``."""
+        batch = int(llr.shape[0])
+        if not llr.flags.c_contiguous:
+            raise ValueError("llr must be C-contiguous")
+        if out is None:
+            out = self.host_outputs(batch)
+        t = ctypes.c_int64()
+        _native.check(_native.load().nrldpc_decode_host_async(
+            self.handle, llr.ctypes.data, batch, out["bits"].ctypes.data, out["iters"].ctypes.data,
+            out["synd"].ctypes.data, out["success"].ctypes.data, out["crc_ok"].ctypes.data,
+            int(chunks), ctypes.byref(t)))
+        return t.value, out
+
+    def host_wait(self, ticket: int) -> None:
+        _native.check(_native.load().nrldpc_host_wait(self.handle, int(ticket)))
+
     def decode_host(self, llr: np.ndarray, chunks: int = 4, out: dict | None = None) -> dict:
         """Synchronous end-to-end decode of HOST buffers through the C ABI
         (H2D copy, kernel, D2H copy pipelined over ``chunks`` sub-batches)."""

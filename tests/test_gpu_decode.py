@@ -243,6 +243,39 @@ def test_out_of_range_host_int8_raises_and_plan_stays_usable(cuda_ok, bg_id, z, 
     _oracle_cmp(bg, bg.m_bg, nr.DecodeConfig(max_iter=4), blocks)
 
 
+def test_async_host_pipeline_matches_sync_and_reports_errors(cuda_ok):
+    """nrldpc_decode_host_async / nrldpc_host_wait: two calls in flight give
+    the synchronous results; a bad input fails its own wait; a third call
+    retires the oldest; the plan keeps working afterwards."""
+    bg = nr.load_basegraph("BG1", 384)
+    cfg = nr.DecodeConfig(max_iter=5, early_stop="syndrome")
+    plan = nr.get_plan(bg, 46, cfg)
+    blocks = []
+    for seed in range(3):
+        _, llr = noisy_llrs(bg, 46, 1.5, 9 + seed, seed=(seed, 77))
+        blocks.append(oracle.quantize_i8(llr, 384))
+    ref = [oracle.decode(b, bg, cfg) for b in blocks]
+    pinned = [torch.from_numpy(b).pin_memory().numpy() for b in blocks]
+    outs = [plan.host_outputs(len(b), pinned=True) for b in blocks]
+    tickets = [plan.decode_host_async(pinned[i], chunks=3, out=outs[i])[0] for i in range(2)]
+    plan.host_wait(tickets[0])
+    t2, _ = plan.decode_host_async(pinned[2], chunks=3, out=outs[2])
+    plan.host_wait(tickets[1])
+    plan.host_wait(t2)
+    plan.host_wait(t2)                                   # already retired: no-op
+    for i in range(3):
+        assert np.array_equal(nr.unpack_bits(outs[i]["bits"], plan.k), ref[i]["bits"]), i
+        assert np.array_equal(outs[i]["iters"], ref[i]["iterations"]), i
+    bad = pinned[0].copy()
+    bad[0, 5] = -128
+    t_bad, _ = plan.decode_host_async(bad, chunks=2, out=outs[0])
+    with pytest.raises(ValueError, match="at most 127"):
+        plan.host_wait(t_bad)
+    t_ok, _ = plan.decode_host_async(pinned[1], chunks=2, out=outs[1])
+    plan.host_wait(t_ok)
+    assert np.array_equal(nr.unpack_bits(outs[1]["bits"], plan.k), ref[1]["bits"])
+
+
 def test_native_library_is_the_compute_path(cuda_ok):
     bg = nr.load_basegraph("BG2", 64)
     nr.decode(np.zeros((4, 3328), np.int8), bg, nr.DecodeConfig(max_iter=2))
