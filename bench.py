@@ -317,6 +317,15 @@ def run_ours(args):
     alg_ops = OPS_PER_EDGE * edges * bg.z * args.iters * B
     achieved = alg_ops / (kern_ms * 1e-3)
     alg_bytes = B * (params.n_c + 4 * plan.words + 4 + 4 + 1 + 1)
+    # DRAM bytes per launch of this kernel from the committed ncu --set full
+    # capture (profiles/); ncu does not run inside the bench
+    traffic, traffic_note = None, "no committed ncu capture"
+    tfile = ROOT / "profiles" / "r01_ncu_decode_traffic.json"
+    if tfile.is_file():
+        tj = json.loads(tfile.read_text())
+        traffic = tj["traffic_bytes_per_launch"]
+        traffic_note = (f"bytes/launch, dram__bytes_read.sum + dram__bytes_write.sum of {tj['kernel']} "
+                        f"({tj['source']}); the algorithmic input alone is {B * params.n_c} bytes")
     peaks_file = ROOT / "MEASURED_PEAKS.json"
     peaks = json.loads(peaks_file.read_text()) if peaks_file.is_file() else {}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
@@ -341,7 +350,8 @@ def run_ours(args):
         "bler": bler, "success_rate": success, "quality": quality,
         "roofline": {
             "bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s",
-            "frac": achieved / peak_ops, "traffic": None,
+            "frac": achieved / peak_ops, "traffic": traffic,
+            "traffic_note": traffic_note,
             "note": f"{OPS_PER_EDGE} algorithmic int ops per edge-update per codeword (SURVEY 8d) x "
                     f"{edges} edges x Z x iterations x B per launch / mean kernel time; peak = measured "
                     f"half2 dual-pipe lane-op rate {lane_peak / 1e12:.2f} T/s (ALU pipe alone "
