@@ -65,13 +65,22 @@ def ebn0_to_sigma(ebn0_db: float, rate_eff: float) -> float:
     return math.sqrt(1.0 / (2.0 * rate_eff * ebn0))
 
 
+_QPLANS: dict = {}
+
+
 def _quant_plan(params):
-    # the quantize kernel only needs (Z, n_c); reuse a tiny plan keyed on them
-    from .basegraph import load_basegraph
-    from .decoder import DecodeConfig, get_plan
-    k_b = params.n_c // params.z - params.rows_used
-    bg = load_basegraph(1 if k_b == 22 else 2, params.z)
-    return get_plan(bg, params.rows_used, DecodeConfig())
+    # the quantize kernel only needs (Z, n_c); reuse one plan per shape (the
+    # lookup is on the per-call path, so it must not rebuild graph tables)
+    import torch
+    key = (params.n_c, params.z, params.rows_used, torch.cuda.current_device())
+    plan = _QPLANS.get(key)
+    if plan is None:
+        from .basegraph import load_basegraph
+        from .decoder import DecodeConfig, get_plan
+        k_b = params.n_c // params.z - params.rows_used
+        bg = load_basegraph(1 if k_b == 22 else 2, params.z)
+        plan = _QPLANS[key] = get_plan(bg, params.rows_used, DecodeConfig(), device=key[3])
+    return plan
 
 
 def quantize(llrs, cfg: QuantConfig, params):

@@ -968,32 +968,87 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
 // With DEMAP the input is received BPSK symbols y and the LLR is formed first
 // exactly as channel.demap_llr does it: (2.0 * y) / (sigma * sigma), float64
 // (channel.py:57-61), with sigma2 = sigma*sigma computed on the host.
+template <typename Tin, int MODE, bool DEMAP>
+__device__ __forceinline__ void quant_one(double v, bool pad, double scale, double clip, double sigma2,
+                                          void* __restrict__ out, long long i) {
+  if (pad) v = 0.0;
+  else if (DEMAP) v = __ddiv_rn(__dmul_rn(2.0, v), sigma2);
+  if (MODE == NRLDPC_INT8) {
+    double q = rint(v * scale);
+    q = fmin(fmax(q, -127.0), 127.0);
+    reinterpret_cast<int8_t*>(out)[i] = (int8_t)q;
+  } else if (MODE == NRLDPC_F16) {
+    double c = fmin(fmax(v, -clip), clip);
+    c = fmin(fmax(c, -65504.0), 65504.0);
+    reinterpret_cast<__half*>(out)[i] = __double2half(c);
+  } else {
+    const double c = fmin(fmax(v, -clip), clip);
+    reinterpret_cast<float*>(out)[i] = __double2float_rn(c);
+  }
+}
+
+// One thread per 8 consecutive output positions of one codeword row (grid:
+// x over the row, y over codewords). Rows whose input is 16-byte aligned take
+// two-to-four 128-bit loads per thread and one packed store; the 2Z punctured
+// head and unaligned shapes (odd Z) use the per-element path. HBM-bound:
+// 8 B (f64) or 4 B (f32) in per position, 1/2/4 B out.
 template <typename Tin, int MODE, bool DEMAP = false>
 __global__ void __launch_bounds__(256) k_quantize(const Tin* __restrict__ in, long long batch, int n_tx,
                                                   int n_c, int two_z, double scale, double clip,
-                                                  void* __restrict__ out, double sigma2 = 1.0) {
-  const long long total = batch * (long long)n_c;
-  const long long stride = (long long)gridDim.x * blockDim.x * 4;
-  for (long long i0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4; i0 < total; i0 += stride) {
+                                                  void* __restrict__ out, double sigma2, int vec) {
+  const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (j0 >= n_c) return;
+  for (long long b = blockIdx.y; b < batch; b += gridDim.y) {
+    const Tin* row = in + b * n_tx;
+    const long long o0 = b * n_c + j0;
+    if (vec && j0 >= two_z && j0 + 8 <= n_c) {
+      double v[8];
+      if (sizeof(Tin) == 8) {
+        const double2* q = reinterpret_cast<const double2*>(row + (j0 - two_z));
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const long long i = i0 + k;
-      if (i >= total) break;
-      const long long b = i / n_c;
-      const int j = (int)(i - b * n_c);
-      double v = j < two_z ? 0.0 : (double)in[b * n_tx + (j - two_z)];
-      if (DEMAP && j >= two_z) v = __ddiv_rn(__dmul_rn(2.0, v), sigma2);
-      if (MODE == NRLDPC_INT8) {
-        double s = rint(v * scale);
-        s = fmin(fmax(s, -127.0), 127.0);
-        reinterpret_cast<int8_t*>(out)[i] = (int8_t)s;
-      } else if (MODE == NRLDPC_F16) {
-        double c = fmin(fmax(v, -clip), clip);
-        c = fmin(fmax(c, -65504.0), 65504.0);
-        reinterpret_cast<__half*>(out)[i] = __double2half(c);
+        for (int k = 0; k < 4; ++k) {
+          const double2 d = __ldcs(q + k);
+          v[2 * k] = d.x;
+          v[2 * k + 1] = d.y;
+        }
       } else {
-        const double c = fmin(fmax(v, -clip), clip);
-        reinterpret_cast<float*>(out)[i] = __double2float_rn(c);
+        const float4* q = reinterpret_cast<const float4*>(row + (j0 - two_z));
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const float4 f = __ldcs(q + k);
+          v[4 * k] = f.x;
+          v[4 * k + 1] = f.y;
+          v[4 * k + 2] = f.z;
+          v[4 * k + 3] = f.w;
+        }
+      }
+      if (MODE == NRLDPC_INT8) {
+        uint32_t lo = 0, hi = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          double x = DEMAP ? __ddiv_rn(__dmul_rn(2.0, v[k]), sigma2) : v[k];
+          double q = rint(x * scale);
+          q = fmin(fmax(q, -127.0), 127.0);
+          const uint32_t byte = (uint32_t)(uint8_t)(int8_t)q;
+          if (k < 4) lo |= byte << (8 * k);
+          else hi |= byte << (8 * (k - 4));
+        }
+        if (vec == 2) {
+          *reinterpret_cast<uint2*>(reinterpret_cast<int8_t*>(out) + o0) = make_uint2(lo, hi);
+        } else {
+          uint32_t* o = reinterpret_cast<uint32_t*>(reinterpret_cast<int8_t*>(out) + o0);
+          o[0] = lo;
+          o[1] = hi;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) quant_one<Tin, MODE, DEMAP>(v[k], false, scale, clip, sigma2, out, o0 + k);
+      }
+    } else {
+      for (int k = 0; k < 8 && j0 + k < n_c; ++k) {
+        const int j = j0 + k;
+        const bool pad = j < two_z;
+        quant_one<Tin, MODE, DEMAP>(pad ? 0.0 : (double)row[j - two_z], pad, scale, clip, sigma2, out, o0 + k);
       }
     }
   }
@@ -1920,13 +1975,24 @@ static int quantize_impl(const nrldpc_plan* plan, const void* llr_in, int in_dty
   const int n_tx = n_c - 2 * plan->z;
   cudaStream_t st = (cudaStream_t)stream;
   NR_CUDA(cudaSetDevice(plan->device));
-  const long long total = batch * (long long)n_c;
-  const long long want = (total + 4 * 256 - 1) / (4 * 256);
-  const int grid = (int)std::min<long long>(want, 148LL * 16);
   const double sigma2 = sigma * sigma;
+  // row-vector path: 16-byte aligned input rows (and int8 output rows of at
+  // least 4-byte alignment: vec 1 = two 32-bit stores, 2 = one 64-bit store)
+  const size_t in_bytes = in_dtype == NRLDPC_IN_F64 ? 8 : 4;
+  const bool in_ok = ((size_t)n_tx * in_bytes) % 16 == 0 && ((size_t)2 * plan->z * in_bytes) % 16 == 0 &&
+                     ((uintptr_t)llr_in & 15) == 0;
+  int vec = 0;
+  if (in_ok) {
+    if (out_mode != NRLDPC_INT8) vec = 1;
+    else if (n_c % 8 == 0 && ((uintptr_t)out & 7) == 0) vec = 2;
+    else if (n_c % 4 == 0 && ((uintptr_t)out & 3) == 0) vec = 1;
+  }
+  const dim3 grid((unsigned)((n_c + 8 * 256 - 1) / (8 * 256)), (unsigned)std::min<int64_t>(batch, 65535));
   auto go = [&](auto k_plain, auto k_demap, auto* typed_in) {
-    if (demap) k_demap<<<grid, 256, 0, st>>>(typed_in, (long long)batch, n_tx, n_c, 2 * plan->z, scale, clip, out, sigma2);
-    else k_plain<<<grid, 256, 0, st>>>(typed_in, (long long)batch, n_tx, n_c, 2 * plan->z, scale, clip, out, 1.0);
+    if (demap)
+      k_demap<<<grid, 256, 0, st>>>(typed_in, (long long)batch, n_tx, n_c, 2 * plan->z, scale, clip, out, sigma2, vec);
+    else
+      k_plain<<<grid, 256, 0, st>>>(typed_in, (long long)batch, n_tx, n_c, 2 * plan->z, scale, clip, out, 1.0, vec);
   };
   if (in_dtype == NRLDPC_IN_F64) {
     const double* in = static_cast<const double*>(llr_in);
