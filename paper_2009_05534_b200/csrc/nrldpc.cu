@@ -1487,11 +1487,11 @@ static cudaError_t launch_shape(const nrldpc_plan* plan, Shape& sh, const int8_t
   }
 }
 
-template <int PREC>
-static cudaError_t launch_float(Shape& sh, int device, const void* llr, long long batch, const KOut& o,
+template <int PREC, int BG>
+static cudaError_t launch_float_bg(Shape& sh, int device, const void* llr, long long batch, const KOut& o,
                                 cudaStream_t st) {
   static bool attr_done[64] = {};
-  auto kern = k_decode_flt<PREC>;
+  auto kern = k_decode_flt<PREC, BG>;
   if (!attr_done[device & 63]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (e != cudaSuccess) return e;
@@ -1519,6 +1519,15 @@ static cudaError_t launch_float(Shape& sh, int device, const void* llr, long lon
   e = cudaGetLastError();
   const cudaError_t f = cudaFreeAsync(ws, st);
   return e != cudaSuccess ? e : f;
+}
+
+// compile-time row bodies for the BG1/BG2 schedules, generic loop otherwise
+template <int PREC>
+static cudaError_t launch_float(int schedule, Shape& sh, int device, const void* llr, long long batch,
+                                const KOut& o, cudaStream_t st) {
+  if (schedule == 1) return launch_float_bg<PREC, 1>(sh, device, llr, batch, o, st);
+  if (schedule == 2) return launch_float_bg<PREC, 2>(sh, device, llr, batch, o, st);
+  return launch_float_bg<PREC, 0>(sh, device, llr, batch, o, st);
 }
 
 extern "C" {
@@ -1879,6 +1888,12 @@ int nrldpc_plan_create(int device, int k_b, int z, int rows_used, const int32_t*
     p->main = choose_shape(p, force && force[0] == '1' ? 1 : 2);
   } else {
     p->main = choose_shape_float(p);
+    if (p->schedule != 0) {
+      // layer units with messages addressed by edge index ([edge][z] workspace)
+      MsgLayout ml{};
+      for (int r = 0; r < p->rows; ++r) ml.mb[r] = (uint32_t)p->base.row_start[r];
+      build_units(p, 0, ml, p->main.kp);
+    }
     if (precision == NRLDPC_F32) {
       const float bf = (float)beta;  // np.float32(beta)
       std::memcpy(&p->main.kp.beta_f, &bf, 4);
@@ -1898,8 +1913,8 @@ int nrldpc_plan_create(int device, int k_b, int z, int rows_used, const int32_t*
     KOut none{};
     const cudaError_t e1 =
         precision == NRLDPC_INT8 ? launch_shape(p, p->main, nullptr, 0, none, nullptr)
-        : precision == NRLDPC_F32 ? launch_float<NRLDPC_F32>(p->main, device, nullptr, 0, none, nullptr)
-                                  : launch_float<NRLDPC_F16>(p->main, device, nullptr, 0, none, nullptr);
+        : precision == NRLDPC_F32 ? launch_float<NRLDPC_F32>(p->schedule, p->main, device, nullptr, 0, none, nullptr)
+                                  : launch_float<NRLDPC_F16>(p->schedule, p->main, device, nullptr, 0, none, nullptr);
     cudaSetDevice(prev);
     if (e1 != cudaSuccess) {
       delete p;
@@ -2029,8 +2044,8 @@ static int decode_impl(nrldpc_plan* plan, const void* llr, int64_t batch, const 
                        cudaStream_t st) {
   if (plan->precision != NRLDPC_INT8) {
     const cudaError_t e = plan->precision == NRLDPC_F32
-                              ? launch_float<NRLDPC_F32>(plan->main, plan->device, llr, batch, o, st)
-                              : launch_float<NRLDPC_F16>(plan->main, plan->device, llr, batch, o, st);
+                              ? launch_float<NRLDPC_F32>(plan->schedule, plan->main, plan->device, llr, batch, o, st)
+                              : launch_float<NRLDPC_F16>(plan->schedule, plan->main, plan->device, llr, batch, o, st);
     if (e != cudaSuccess) return cuda_fail(e, "decode launch");
     return NRLDPC_OK;
   }

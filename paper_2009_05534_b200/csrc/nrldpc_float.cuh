@@ -69,6 +69,59 @@ struct FOps<NRLDPC_F16> {
   }
 };
 
+// One row of a compile-time (BG1/BG2) layer unit in the float engines,
+// split like the int8 RowWork: pro() touches only this thread's own state
+// (graph tables, edge addresses, its messages from the global workspace), so
+// it runs before the barrier that closes the previous layer; main() reads
+// the posteriors.
+template <int PREC, int W>
+struct FRow {
+  using F = FOps<PREC>;
+  uint32_t off[W], t[W], neg[W], msg[W];
+  uint32_t m1, m2, S, b1, b2;
+  uint32_t* Me;  // this row's first edge: edge j at Me[j * Z]
+  __device__ __forceinline__ void pro(const KParams& p, uint32_t tq, uint32_t e0, uint32_t zl, uint32_t ZL,
+                                      uint32_t* Mg, bool active) {
+    uint32_t tsh[W], tcb[W];
+    load_row_tables<W>(p, tq, W, tsh, tcb);
+    Me = Mg + (long long)e0 * p.z;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      off[j] = edge_offset(tsh[j], tcb[j], zl, ZL);
+      msg[j] = active ? Me[(long long)j * p.z] : 0u;
+    }
+  }
+  __device__ __forceinline__ void main(const uint8_t* Lg, uint32_t beta) {
+    m1 = F::sat();
+    m2 = F::sat();
+    S = 0;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      const uint32_t lv = *reinterpret_cast<const uint32_t*>(Lg + off[j]);
+      t[j] = F::sub_clamp(lv, msg[j]);             // decoder.py:300
+      const uint32_t a = F::absv(t[j]);
+      neg[j] = F::neg_mask(t[j]);                  // lvc < 0 (-0 is not negative)
+      m2 = F::minv(m2, F::maxv(m1, a));            // kernels.py:247-250
+      m1 = F::minv(m1, a);
+      S ^= neg[j];
+    }
+    b1 = F::mul(beta, m1);                         // dtype(beta) * m
+    b2 = F::mul(beta, m2);
+  }
+  __device__ __forceinline__ void scatter(uint8_t* Lg, const KParams& p, bool active) {
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      const uint32_t eq = F::eq_mask(F::absv(t[j]), m1);        // the argmin edge (ties: m1 == m2)
+      const uint32_t mag = (eq & b2) | (~eq & b1);
+      const uint32_t out = mag ^ ((S ^ neg[j]) & F::sign);       // -mag flips the sign bit
+      if (active) {
+        Me[(long long)j * p.z] = out;
+        *reinterpret_cast<uint32_t*>(Lg + off[j]) = F::add_clamp(t[j], out);  // decoder.py:318
+      }
+    }
+  }
+};
+
 struct FltState {
   int synd[2];
   float minabs[2];
@@ -76,7 +129,7 @@ struct FltState {
   uint32_t accept[2];
 };
 
-template <int PREC>
+template <int PREC, int BG = 0>
 __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KParams p,
                                                     const void* __restrict__ llr,
                                                     uint32_t* __restrict__ ws, KOut o) {
@@ -142,6 +195,35 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
 
   const uint32_t beta = p.beta_f;
   for (int it = 1; it <= p.max_iter; ++it) {
+   if constexpr (BG != 0) {
+    // host-built layer units (KParams::unit_a/b, edge indices for messages)
+    bool bar_prev = false;
+#pragma unroll 1
+    for (int u = 0; u < p.n_units; ++u) {
+      const uint4 A = p.unit_a[u];
+      const uint4 B = p.unit_b[u];
+      dispatch_unit<BG, 0>(A.x, [&](auto WA, auto WB) {
+        constexpr int wa = decltype(WA)::value, wb = decltype(WB)::value;
+        FRow<PREC, wa> ra;
+        ra.pro(p, A.z, A.w, zl, ZL, Mg, active);
+        if constexpr (wb == 0) {
+          if (bar_prev) __syncthreads();
+          ra.main(Lg, beta);
+          ra.scatter(Lg, p, active);
+        } else {
+          FRow<PREC, wb> rb;
+          rb.pro(p, B.x, B.y, zl, ZL, Mg, active);
+          if (bar_prev) __syncthreads();
+          ra.main(Lg, beta);
+          rb.main(Lg, beta);
+          ra.scatter(Lg, p, active);
+          rb.scatter(Lg, p, active);
+        }
+      });
+      bar_prev = A.y != 0;
+    }
+    if (bar_prev) __syncthreads();
+   } else {
     for (int r = 0; r < p.rows; ++r) {
       const int e0 = p.row_start[r];
       const int w = p.row_start[r + 1] - e0;
@@ -178,6 +260,7 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
       }
       __syncthreads();
     }
+   }
     const bool last = it == p.max_iter;
     if (!(p.early_stop != NRLDPC_STOP_NONE || p.trace || last)) continue;
 
