@@ -551,6 +551,18 @@ struct RegMsg {
 #pragma unroll
     for (int i = 0; i < 4; ++i) r5[i] = 0x80808080u;
   }
+  // zero (biased 0x80) one lane's bytes of every register message
+  __device__ __forceinline__ void reset_lane(uint32_t keep) {
+    const uint32_t z = 0x80808080u & ~keep;
+#pragma unroll
+    for (int k = 0; k < (nq > 0 ? nq : 1); ++k)
+#pragma unroll
+      for (int i = 0; i < 10; ++i) q[k][i] = (q[k][i] & keep) | z;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) r4[i] = (r4[i] & keep) | z;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) r5[i] = (r5[i] & keep) | z;
+  }
   // rows come in twos: after rows (2k, 2k+1) swap the head pair with the
   // tail pair (nq == 4); nq == 2 needs no movement at all
   __device__ __forceinline__ void rotate2() {
@@ -704,7 +716,8 @@ __device__ __forceinline__ void write_bits(const KParams& p, const uint8_t* __re
 template <int LANES>
 __device__ __forceinline__ void write_bits_warp(const KParams& p, const uint8_t* __restrict__ Lg, int z,
                                                 const int (&need)[2], long long cw0,
-                                                uint32_t* __restrict__ bits) {
+                                                uint32_t* __restrict__ bits, long long cw1 = -1) {
+  if (cw1 < 0) cw1 = cw0 + 1;
   const int K = p.k_b * p.z;
   const int lid = z & 31;
   for (int wi = z >> 5; wi < p.words; wi += p.z >> 5) {
@@ -714,7 +727,7 @@ __device__ __forceinline__ void write_bits_warp(const KParams& p, const uint8_t*
     const uint32_t wb = __ballot_sync(0xFFFFFFFFu, ((u >> 8) & 0xFFu) < 128u);
     if (lid == 0) {
       if (need[0]) bits[cw0 * p.words + wi] = wa;
-      if (LANES == 2 && need[1]) bits[(cw0 + 1) * p.words + wi] = wb;
+      if (LANES == 2 && need[1]) bits[cw1 * p.words + wi] = wb;
     }
   }
 }
@@ -960,6 +973,203 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
     // block-wide vote: provably uniform, so the layer loop stays on the
     // uniform datapath (graph tables in uniform registers)
     if (__syncthreads_and(!p.trace && cta->n_done >= cta->n_valid)) break;
+  }
+}
+
+// ---- lane-refill decode (early-stop modes) --------------------------------
+// The pair kernel above runs a CTA until both of its codewords stop, so in
+// syndrome/CRC modes a lane idles once its codeword converges. This
+// persistent variant refills a lane as soon as its codeword stops: the CTA
+// writes that codeword's results, takes the next codeword index from a
+// global counter, loads it into the lane's bytes of L and zeroes the lane's
+// messages, while the other lane keeps iterating. Each lane counts its own
+// iterations; every codeword runs exactly the reference's schedule
+// (decoder.py:486-540), so results are unchanged. One group of Z threads per
+// CTA (Z % 32 == 0), two lanes, absolute addressing; not for traced runs.
+struct LaneState {
+  long long cw[2];  // codeword in each lane (-1: idle)
+  int it[2];        // iterations run on it
+  int pad[2];
+};
+
+template <int BG, int MAXW, int NREG>
+__global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const __grid_constant__ KParams p,
+                                                                          const int8_t* __restrict__ llr, KOut o) {
+  constexpr int LANES = 2;
+  constexpr bool ABS = true;
+  extern __shared__ __align__(16) uint8_t smem[];
+  LaneState* ls = reinterpret_cast<LaneState*>(smem);  // the (unused) beta-table area
+  CtaState* cta = reinterpret_cast<CtaState*>(smem + kLutBytes);
+  GroupState& gs = *reinterpret_cast<GroupState*>(smem + kLutBytes + kCtaBytes);
+  const uint32_t data_off = data_offset(1);
+  const int tid = threadIdx.x;
+  const int z = tid;
+  const bool st_ok = true;
+  const uint32_t ZL = (uint32_t)p.z * LANES;
+  const uint32_t zl = (uint32_t)z * LANES;
+  const long long n_c = (long long)p.n_blocks * p.z;
+  uint8_t* Lg = smem + data_off;
+  uint8_t* Mz = Lg + p.l_bytes + (uint32_t)z * p.m_stride;
+  if ((uint32_t)__cvta_generic_to_shared(Lg) != p.abs_base) __trap();
+
+  if (tid == 0) {
+    cta->kc[0] = p.magic;
+    cta->kc[1] = p.one;
+    cta->kc[2] = p.beta_h;
+    cta->kc[3] = p.ndelta_h;
+    cta->kc[4] = p.c_h;
+    for (int l = 0; l < 2; ++l) {
+      const long long c = 2LL * blockIdx.x + l;
+      ls->cw[l] = c < p.batch ? c : -1;
+      ls->it[l] = 0;
+      gs.synd[l] = 0;
+      gs.minabs[l] = 255;
+      gs.done[l] = 0;
+      gs.accept[l] = 0;
+    }
+  }
+  // messages: all zero (biased)
+  {
+    uint4* m4 = reinterpret_cast<uint4*>(Lg + p.l_bytes);
+    const uint4 zero4 = make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);
+    for (uint32_t k = z; k < (p.m_bytes >> 4); k += p.z) m4[k] = zero4;
+  }
+  __syncthreads();
+
+  // load one lane's codeword (int8 -> biased byte) into its bytes of L:
+  // 16 positions per thread and step when the row is 16-byte aligned (one
+  // LDG.128, byte-interleaved into the other lane's bytes with PRMT)
+  auto load_lane = [&](int l, long long cw) {
+    uint32_t bad = 0;
+    const int8_t* src = llr + cw * n_c;
+    if (p.vec_load) {
+      const uint4* row = reinterpret_cast<const uint4*>(src);
+      uint4* dst = reinterpret_cast<uint4*>(Lg);
+      const uint32_t keep = l ? 0x00FF00FFu : 0xFF00FF00u;
+      for (int k = z; k < (int)(n_c >> 4); k += p.z) {
+        uint4 a = row[k];
+        a.x ^= 0x80808080u; a.y ^= 0x80808080u; a.z ^= 0x80808080u; a.w ^= 0x80808080u;
+        bad |= (a.x - 0x01010101u) & ~a.x; bad |= (a.y - 0x01010101u) & ~a.y;
+        bad |= (a.z - 0x01010101u) & ~a.z; bad |= (a.w - 0x01010101u) & ~a.w;
+        // spread 4 bytes to the lane's byte of 4 positions: 0x5140 -> lane 0,
+        // then shift up by 8 for lane 1
+        const uint32_t in4[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint4 d = dst[2 * k + h];
+          const uint32_t u0 = __byte_perm(in4[2 * h], 0, 0x4140), u1 = __byte_perm(in4[2 * h], 0, 0x4342);
+          const uint32_t u2 = __byte_perm(in4[2 * h + 1], 0, 0x4140), u3 = __byte_perm(in4[2 * h + 1], 0, 0x4342);
+          const int sh = 8 * l;
+          d.x = (d.x & keep) | ((u0 << sh) & ~keep);
+          d.y = (d.y & keep) | ((u1 << sh) & ~keep);
+          d.z = (d.z & keep) | ((u2 << sh) & ~keep);
+          d.w = (d.w & keep) | ((u3 << sh) & ~keep);
+          dst[2 * k + h] = d;
+        }
+      }
+      bad &= 0x80808080u;
+    } else {
+      for (long long n = z; n < n_c; n += p.z) {
+        const int8_t x = src[n];
+        bad |= (x == -128);
+        Lg[n * 2 + l] = (uint8_t)x ^ 0x80u;
+      }
+    }
+    if (bad && o.status) atomicOr(o.status, 1);
+  };
+  long long cw[2] = {ls->cw[0], ls->cw[1]};
+  for (int l = 0; l < 2; ++l) {
+    if (cw[l] >= 0) load_lane(l, cw[l]);
+    else for (long long n = z; n < n_c; n += p.z) Lg[n * 2 + l] = 0x80u;
+  }
+  __syncthreads();
+
+  const Consts kc{lds_u32(&cta->kc[0]), lds_u32(&cta->kc[1]), lds_u32(&cta->kc[2]), lds_u32(&cta->kc[3]),
+                  lds_u32(&cta->kc[4])};
+  const RowCtx rc{zl, ZL, Lg, Mz, (uint32_t)__cvta_generic_to_shared(Mz), nullptr, kc, st_ok};
+  RegMsg<NREG> rm;
+  rm.init();
+  int it[2] = {0, 0};
+  while (cw[0] >= 0 || cw[1] >= 0) {
+    one_iteration<BG, MAXW, LANES, NREG, ABS>(p, rc, rm);
+    bool act[2], last[2];
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+      act[l] = cw[l] >= 0;
+      it[l] += act[l] ? 1 : 0;
+      last[l] = act[l] && it[l] == p.max_iter;
+    }
+    {
+      int wc[2], ma[2];
+      local_check<BG, MAXW, LANES, ABS>(p, zl, ZL, Lg, wc, ma, !last[0] && !last[1], act[0], act[1]);
+#pragma unroll
+      for (int l = 0; l < 2; ++l) {
+        if (wc[l]) atomicAdd(&gs.synd[l], wc[l]);
+        atomicMin(&gs.minabs[l], ma[l]);
+      }
+    }
+    __syncthreads();
+    int cand[2], fin[2];
+#pragma unroll
+    for (int l = 0; l < 2; ++l) cand[l] = act[l] && gs.synd[l] == 0 && gs.minabs[l] > 0;
+    if (p.early_stop == NRLDPC_STOP_CRC) {
+#pragma unroll
+      for (int l = 0; l < 2; ++l) {
+        if (cand[l]) {
+          const uint32_t part = p.crc_tab ? crc_partial<LANES>(p, Lg, z, l) : 1u;
+          if (part) atomicXor(reinterpret_cast<unsigned int*>(&gs.accept[l]), part);
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int l = 0; l < 2; ++l) cand[l] = cand[l] && p.crc_tab != nullptr && gs.accept[l] == 0;
+    }
+#pragma unroll
+    for (int l = 0; l < 2; ++l) fin[l] = last[l] && !cand[l];
+    const int need[2] = {cand[0] || fin[0], cand[1] || fin[1]};
+    if (need[0] || need[1]) {
+      write_bits_warp<LANES>(p, Lg, z, need, cw[0], o.bits, cw[1]);
+      if (z == 0) {
+#pragma unroll
+        for (int l = 0; l < 2; ++l) {
+          if (!need[l]) continue;
+          const long long c = cw[l];
+          o.iters[c] = cand[l] ? it[l] : p.max_iter;
+          o.synd[c] = cand[l] ? 0 : gs.synd[l];
+          o.success[c] = cand[l] ? 1 : 0;
+          if (o.crc_ok) o.crc_ok[c] = cand[l] ? 1 : 0;
+          // the next codeword for this lane
+          const long long nxt = 2LL * gridDim.x + atomicAdd(o.work, 1);
+          ls->cw[l] = nxt < p.batch ? nxt : -1;
+        }
+      }
+    }
+    __syncthreads();
+    if (z == 0) {
+#pragma unroll
+      for (int l = 0; l < 2; ++l) {
+        gs.synd[l] = 0;
+        gs.minabs[l] = 255;
+        gs.accept[l] = 0;
+      }
+    }
+    if (need[0] || need[1]) {
+#pragma unroll
+      for (int l = 0; l < 2; ++l) {
+        if (!need[l]) continue;
+        cw[l] = ls->cw[l];
+        it[l] = 0;
+        if (cw[l] >= 0) {
+          load_lane(l, cw[l]);
+          // this lane's messages back to zero (bytes l of every 16-bit pair)
+          const uint32_t keep = l ? 0x00FF00FFu : 0xFF00FF00u;
+          uint32_t* m32 = reinterpret_cast<uint32_t*>(Lg + p.l_bytes);
+          for (uint32_t k = z; k < (p.m_bytes >> 2); k += p.z) m32[k] = (m32[k] & keep) | (0x80808080u & ~keep);
+          rm.reset_lane(keep);
+        }
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -1461,11 +1671,63 @@ Shape choose_shape(const nrldpc_plan* p, int max_lanes) {
 
 }  // namespace
 
+// Persistent lane-refill launch (early-stop modes, single-group pair shapes):
+// one CTA per resident slot, each refilling its lanes from a per-launch
+// codeword counter.
+template <int BG, int MAXW, int NREG>
+static cudaError_t launch_refill(Shape& sh, int device, const int8_t* llr, long long batch, const KOut& o,
+                                 cudaStream_t st) {
+  static bool attr_done[64] = {};
+  static int occ_cache[64] = {}, sms[64] = {};
+  auto kern = k_decode_i8_refill<BG, MAXW, NREG>;
+  const int d = device & 63;
+  if (!attr_done[d]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cache[d], kern, sh.threads, sh.smem);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms[d], cudaDevAttrMultiProcessorCount, device);
+    if (e != cudaSuccess) return e;
+    if (occ_cache[d] < 1) occ_cache[d] = 1;
+    attr_done[d] = true;
+  }
+  if (!llr) return cudaSuccess;
+  KParams kp = sh.kp;
+  kp.batch = batch;
+  kp.trace = 0;
+  kp.vec_load = ((long long)kp.n_blocks * kp.z) % 16 == 0 && ((uintptr_t)llr & 15) == 0;
+  const long long pairs = (batch + 1) / 2;
+  const long long grid = std::min<long long>(pairs, (long long)occ_cache[d] * sms[d]);
+  int32_t* work = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&work), sizeof(int32_t), st);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(work, 0, sizeof(int32_t), st);
+  if (e == cudaSuccess) {
+    KOut oo = o;
+    oo.work = work;
+    kern<<<(unsigned)grid, sh.threads, sh.smem, st>>>(kp, llr, oo);
+    ++g_launches;
+    e = cudaGetLastError();
+  }
+  const cudaError_t f = cudaFreeAsync(work, st);
+  return e != cudaSuccess ? e : f;
+}
+
 static cudaError_t launch_shape(const nrldpc_plan* plan, Shape& sh, const int8_t* in, int64_t batch,
                                 const KOut& o, cudaStream_t st) {
   if (sh.threads == 0) return cudaErrorInvalidConfiguration;  // no feasible shape
   const bool two = sh.lanes == 2;
   const int dev = plan->device;
+  // early-stop modes without a trace: refill lanes as codewords stop
+  const bool refill = plan->early_stop != NRLDPC_STOP_NONE && o.trace_w == nullptr && sh.abs && two &&
+                      sh.groups == 1 && plan->z % 32 == 0 && !getenv("NRLDPC_NO_REFILL");
+  if (refill && (in == nullptr || batch > 2)) {
+    cudaError_t e = cudaSuccess;
+    if (plan->schedule == 1 && sh.nreg == 6) e = launch_refill<1, 19, 6>(sh, dev, in, batch, o, st);
+    else if (plan->schedule == 1 && sh.nreg == 0) e = launch_refill<1, 19, 0>(sh, dev, in, batch, o, st);
+    else if (plan->schedule == 2 && sh.nreg == 0) e = launch_refill<2, 10, 0>(sh, dev, in, batch, o, st);
+    else goto plain;
+    if (in != nullptr || e != cudaSuccess) return e;
+  }
+plain:
   switch (plan->schedule) {
     case 1:
       if (!two) return launch_i8<1, 19, 1>(sh, dev, in, batch, o, st);

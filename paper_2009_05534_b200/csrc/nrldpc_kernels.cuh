@@ -86,6 +86,7 @@ struct KOut {
   int32_t* trace_w;
   float* trace_m;
   int32_t* status;
+  int32_t* work;  // lane-refill kernel: next-codeword counter (zeroed per launch)
 };
 
 __device__ __forceinline__ uint32_t h2u(half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
