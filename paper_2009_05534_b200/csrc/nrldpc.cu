@@ -1163,8 +1163,16 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const 
           load_lane(l, cw[l]);
           // this lane's messages back to zero (bytes l of every 16-bit pair)
           const uint32_t keep = l ? 0x00FF00FFu : 0xFF00FF00u;
-          uint32_t* m32 = reinterpret_cast<uint32_t*>(Lg + p.l_bytes);
-          for (uint32_t k = z; k < (p.m_bytes >> 2); k += p.z) m32[k] = (m32[k] & keep) | (0x80808080u & ~keep);
+          const uint32_t zb = 0x80808080u & ~keep;
+          uint4* m4 = reinterpret_cast<uint4*>(Lg + p.l_bytes);
+          for (uint32_t k = z; k < (p.m_bytes >> 4); k += p.z) {
+            uint4 v = m4[k];
+            v.x = (v.x & keep) | zb;
+            v.y = (v.y & keep) | zb;
+            v.z = (v.z & keep) | zb;
+            v.w = (v.w & keep) | zb;
+            m4[k] = v;
+          }
           rm.reset_lane(keep);
         }
       }

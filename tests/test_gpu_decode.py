@@ -276,6 +276,31 @@ def test_async_host_pipeline_matches_sync_and_reports_errors(cuda_ok):
     assert np.array_equal(nr.unpack_bits(outs[1]["bits"], plan.k), ref[1]["bits"])
 
 
+@pytest.mark.parametrize("bg_id,z,stop,ebn0", [("BG1", 384, "syndrome", 2.0), ("BG2", 384, "crc", 1.0),
+                                               ("BG1", 256, "syndrome", 1.5), ("BG2", 96, "syndrome", 0.8)])
+def test_lane_refill_matches_pair_kernel_and_oracle(cuda_ok, bg_id, z, stop, ebn0, monkeypatch):
+    """Early-stop modes run the persistent lane-refill kernel; it must give
+    the pair kernel's (and the oracle's) results codeword for codeword."""
+    bg = nr.load_basegraph(bg_id, z)
+    params = nr.code_params(bg, z, bg.m_bg)
+    rng = np.random.default_rng(z)
+    if stop == "crc":
+        msgs = np.stack([nr.crc_attach(rng.integers(0, 2, params.k - 24, dtype=np.uint8), k=params.k)
+                         for _ in range(301)])
+        tx = nr.encode_batch(msgs, bg, z, bg.m_bg)[:, 2 * z:]
+        sigma = nr.ebn0_to_sigma(ebn0, params.k / params.n_tx)
+        llr = nr.demap_llr(nr.bpsk_awgn(tx, sigma, rng), sigma)
+    else:
+        _, llr = noisy_llrs(bg, bg.m_bg, ebn0, 301, seed=(z, 3))
+    blocks = oracle.quantize_i8(llr, z)
+    cfg = nr.DecodeConfig(max_iter=12, early_stop=stop)
+    res = _oracle_cmp(bg, bg.m_bg, cfg, blocks)                 # refill path (default)
+    monkeypatch.setenv("NRLDPC_NO_REFILL", "1")
+    res2 = nr.decode(blocks, bg, cfg)                           # pair kernel
+    assert np.array_equal(res.bits, res2.bits) and np.array_equal(res.iterations, res2.iterations)
+    assert len(set(res.iterations.tolist())) > 1                # lanes really refilled at different times
+
+
 def test_native_library_is_the_compute_path(cuda_ok):
     bg = nr.load_basegraph("BG2", 64)
     nr.decode(np.zeros((4, 3328), np.int8), bg, nr.DecodeConfig(max_iter=2))
