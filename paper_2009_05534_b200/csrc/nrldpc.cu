@@ -507,7 +507,7 @@ __device__ __forceinline__ void dispatch_unit(uint32_t code, F&& f) {
   if constexpr (BG == 1) {
     if (wge(c, 256)) {
       if (false) {}
-      NR_U(5, 5); NR_U(5, 4); NR_U(6, 6); NR_U(4, 5); NR_U(6, 5);
+      NR_U(5, 5); NR_U(5, 4); NR_U(6, 6); NR_U(6, 5);
     } else {
       if (false) {}
       NR_U(7, 0); NR_U(6, 0); NR_U(9, 0); NR_U(10, 0); NR_U(8, 0); NR_U(5, 0); NR_U(4, 0);
@@ -521,7 +521,7 @@ __device__ __forceinline__ void dispatch_unit(uint32_t code, F&& f) {
   } else {
     if (wge(c, 256)) {
       if (false) {}
-      NR_U(4, 4); NR_U(4, 3); NR_U(5, 4); NR_U(5, 3); NR_U(3, 4);
+      NR_U(4, 4); NR_U(4, 3); NR_U(5, 4); NR_U(5, 3);
     } else {
       if (false) {}
       NR_U(4, 0); NR_U(5, 0); NR_U(6, 0); NR_U(8, 0); NR_U(10, 0); NR_U(3, 0);
@@ -1567,8 +1567,14 @@ void build_units(const nrldpc_plan* p, int nreg, const MsgLayout& ml, KParams& k
     if (p->schedule != 0 && !b.bar_after[r] && r + 1 < p->rows) {
       const int wb = b.row_start[r + 2] - b.row_start[r + 1];
       if (fused_pair(p->schedule, wa, wb)) {
-        kp.unit_a[n] = make_uint4((uint32_t)(wa | wb << 8), b.bar_after[r + 1], ta, ml.mb[r]);
-        kp.unit_b[n] = make_uint4(b.tab_start[r + 1] / 4u, ml.mb[r + 1], ml.mh[r], ml.mh[r + 1]);
+        // the two rows share no column, so their order inside the fused body
+        // is free: the heavier row goes first and (4,5) runs on the (5,4)
+        // body, (3,4) on (4,3) (fewer bodies in the hot loop)
+        const int f = wa < wb ? 1 : 0;  // row r + f becomes row a
+        const int ra = r + f, rb = r + 1 - f;
+        kp.unit_a[n] = make_uint4((uint32_t)(std::max(wa, wb) | std::min(wa, wb) << 8), b.bar_after[r + 1],
+                                  b.tab_start[ra] / 4u, ml.mb[ra]);
+        kp.unit_b[n] = make_uint4(b.tab_start[rb] / 4u, ml.mb[rb], ml.mh[ra], ml.mh[rb]);
         ++n;
         r += 2;
         continue;
