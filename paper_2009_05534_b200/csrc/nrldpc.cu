@@ -611,9 +611,8 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
     }
     // The remaining rows run as host-built units (a single row, or two
     // consecutive column-disjoint rows fused into one basic block) with
-    // precomputed byte offsets; each unit's descriptor is loaded one unit
-    // ahead so the dispatch after a barrier does not wait on the constant
-    // cache.
+    // precomputed offsets; each unit's dispatch code is loaded one unit
+    // ahead so the dispatch does not wait on the constant cache.
     uint32_t ncode = p.unit_a[0].x;
     // The barrier that closes a layer runs inside the next unit, after its
     // thread-private prologue (tables, addresses, own messages) and before
