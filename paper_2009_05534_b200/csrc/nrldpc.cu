@@ -76,6 +76,9 @@ __host__ __device__ constexpr uint32_t data_offset(int groups) {
 }
 
 // (z + s) mod Z for one edge, as a byte offset into the group's L array.
+// codeword-load steps whose global loads are issued together
+constexpr int kLoadBatch = 4;
+
 __device__ __forceinline__ uint32_t edge_offset(uint32_t shift, uint32_t colbase, uint32_t zl, uint32_t ZL) {
   uint32_t a = zl + shift;
   a = min(a, a - ZL);  // unsigned: picks a-ZL only when a >= ZL  (one VIADDMNMX)
@@ -821,13 +824,26 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
       const int chunks = (int)(n_c >> 4);
       const uint4* rowA = reinterpret_cast<const uint4*>(llr + cw0 * n_c);
       const uint4* rowB = reinterpret_cast<const uint4*>(llr + (cw0 + 1) * n_c);
-      for (int k = z; k < chunks; k += p.z) {
-        uint4 a = lane_valid[0] ? rowA[k] : make_uint4(0, 0, 0, 0);
+      // kLoadBatch steps' loads are issued before any is consumed: one HBM
+      // round trip per batch instead of one per step
+      for (int k0 = z; k0 < chunks; k0 += kLoadBatch * p.z) {
+        uint4 ra[kLoadBatch], rb[kLoadBatch];
+#pragma unroll
+        for (int u = 0; u < kLoadBatch; ++u) {
+          const int k = k0 + u * p.z;
+          ra[u] = lane_valid[0] && k < chunks ? rowA[k] : make_uint4(0, 0, 0, 0);
+          rb[u] = LANES == 2 && lane_valid[1] && k < chunks ? rowB[k] : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < kLoadBatch; ++u) {
+        const int k = k0 + u * p.z;
+        if (k >= chunks) break;
+        uint4 a = ra[u];
         a.x ^= 0x80808080u; a.y ^= 0x80808080u; a.z ^= 0x80808080u; a.w ^= 0x80808080u;
         bad |= (a.x - 0x01010101u) & ~a.x; bad |= (a.y - 0x01010101u) & ~a.y;
         bad |= (a.z - 0x01010101u) & ~a.z; bad |= (a.w - 0x01010101u) & ~a.w;
         if (LANES == 2) {
-          uint4 b = lane_valid[1] ? rowB[k] : make_uint4(0, 0, 0, 0);
+          uint4 b = rb[u];
           b.x ^= 0x80808080u; b.y ^= 0x80808080u; b.z ^= 0x80808080u; b.w ^= 0x80808080u;
           if (lane_valid[1]) {
             bad |= (b.x - 0x01010101u) & ~b.x; bad |= (b.y - 0x01010101u) & ~b.y;
@@ -840,6 +856,7 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
                               __byte_perm(a.w, b.w, 0x5140), __byte_perm(a.w, b.w, 0x7362));
         } else {
           reinterpret_cast<uint4*>(Lg)[k] = a;
+        }
         }
       }
       bad &= 0x80808080u;
@@ -1045,8 +1062,19 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const 
       const uint4* row = reinterpret_cast<const uint4*>(src);
       uint4* dst = reinterpret_cast<uint4*>(Lg);
       const uint32_t keep = l ? 0x00FF00FFu : 0xFF00FF00u;
-      for (int k = z; k < (int)(n_c >> 4); k += p.z) {
-        uint4 a = row[k];
+      const int chunks = (int)(n_c >> 4);
+      for (int k0 = z; k0 < chunks; k0 += kLoadBatch * p.z) {
+        uint4 ra[kLoadBatch];
+#pragma unroll
+        for (int u = 0; u < kLoadBatch; ++u) {
+          const int k = k0 + u * p.z;
+          ra[u] = k < chunks ? row[k] : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < kLoadBatch; ++u) {
+        const int k = k0 + u * p.z;
+        if (k >= chunks) break;
+        uint4 a = ra[u];
         a.x ^= 0x80808080u; a.y ^= 0x80808080u; a.z ^= 0x80808080u; a.w ^= 0x80808080u;
         bad |= (a.x - 0x01010101u) & ~a.x; bad |= (a.y - 0x01010101u) & ~a.y;
         bad |= (a.z - 0x01010101u) & ~a.z; bad |= (a.w - 0x01010101u) & ~a.w;
@@ -1064,6 +1092,7 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const 
           d.z = (d.z & keep) | ((u2 << sh) & ~keep);
           d.w = (d.w & keep) | ((u3 << sh) & ~keep);
           dst[2 * k + h] = d;
+        }
         }
       }
       bad &= 0x80808080u;
@@ -1304,6 +1333,42 @@ __global__ void __launch_bounds__(512) k_alu_peak(uint32_t* out, int iters, uint
 
 // ---------------------------------------------------------------------------
 // Host side
+
+// Stream-ordered scratch (lane-refill work counters, float-engine message
+// workspaces) comes from a library-private pool per device. Reuse of a freed
+// block is limited to orderings the caller's own streams/events establish:
+// with the default pool's internal-dependency reuse, a launch on stream B
+// could be made to wait for an earlier launch on stream A whose block it
+// recycles, which serialises independent batches on separate streams. The
+// release threshold keeps freed blocks cached across synchronisations.
+cudaError_t scratch_alloc(void** ptr, size_t bytes, int device, cudaStream_t st) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  cudaMemPool_t pool;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    cudaMemPool_t& slot = pools[device & 63];
+    if (!slot) {
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = device;
+      cudaError_t e = cudaMemPoolCreate(&slot, &props);
+      int off = 0;
+      uint64_t keep = ~0ull;
+      if (e == cudaSuccess) e = cudaMemPoolSetAttribute(slot, cudaMemPoolReuseAllowOpportunistic, &off);
+      if (e == cudaSuccess) e = cudaMemPoolSetAttribute(slot, cudaMemPoolReuseAllowInternalDependencies, &off);
+      if (e == cudaSuccess) e = cudaMemPoolSetAttribute(slot, cudaMemPoolAttrReleaseThreshold, &keep);
+      if (e != cudaSuccess) {
+        if (slot) cudaMemPoolDestroy(slot);
+        slot = nullptr;
+        return e;
+      }
+    }
+    pool = slot;
+  }
+  return cudaMallocFromPoolAsync(ptr, bytes, pool, st);
+}
 
 // One launch configuration of the decode kernel.
 struct Shape {
@@ -1710,7 +1775,7 @@ static cudaError_t launch_refill(Shape& sh, int device, const int8_t* llr, long 
   const long long pairs = (batch + 1) / 2;
   const long long grid = std::min<long long>(pairs, (long long)occ_cache[d] * sms[d]);
   int32_t* work = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&work), sizeof(int32_t), st);
+  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&work), sizeof(int32_t), device, st);
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(work, 0, sizeof(int32_t), st);
   if (e == cudaSuccess) {
@@ -1787,7 +1852,7 @@ static cudaError_t launch_float_bg(Shape& sh, int device, const void* llr, long 
   // messages: stream-ordered workspace, [group][edge][z] x 4 bytes
   uint32_t* ws = nullptr;
   const size_t ws_bytes = (size_t)grid * sh.groups * kp.n_edges * kp.z * 4;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws), ws_bytes, st);
+  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&ws), ws_bytes, device, st);
   if (e != cudaSuccess) return e;
   kern<<<(unsigned)grid, sh.threads, sh.smem, st>>>(kp, llr, ws, o);
   ++g_launches;
@@ -1858,7 +1923,7 @@ int nrldpc_decode_flooding(nrldpc_plan* plan, const void* llr, int64_t batch, ui
   const size_t smem = 2 * n_c * 4;
   const int threads = (plan->z + 31) / 32 * 32;
   void* ws = nullptr;
-  NR_CUDA(cudaMallocAsync(&ws, (size_t)batch * plan->n_edges * plan->z * 4, st));
+  NR_CUDA(scratch_alloc(&ws, (size_t)batch * plan->n_edges * plan->z * 4, plan->device, st));
   KOut o{bits, iters, synd, success, crc_ok, trace_w, trace_m, nullptr};
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -485,3 +485,51 @@ def test_acceptance_layered_needs_fewer_iterations_than_flooding(cuda_ok):
         flo_ok += int(flo.success.sum())
     assert lay_ok >= 0.99 * 2000 and flo_ok >= 0.99 * 2000
     assert np.mean(lay_it) <= 0.65 * np.mean(flo_it)
+
+
+@pytest.mark.parametrize("prec,stop", [("int8", "syndrome"), ("f16", "none"), ("f32", "syndrome")])
+def test_scratch_paths_capture_and_concurrent_streams(cuda_ok, prec, stop):
+    """Launches that take stream-ordered scratch from the library pool (the
+    lane-refill work counter, float message workspaces) work inside a CUDA
+    graph capture and concurrently on two streams."""
+    bg = nr.load_basegraph("BG1", 384)
+    cfg = nr.DecodeConfig(max_iter=8, early_stop=stop, precision=prec)
+    params = nr.code_params(bg, 384, 46)
+    _, llr = noisy_llrs(bg, 46, 2.5, 6, seed=(len(prec), len(stop), 5))
+    blocks = nr.quantize(llr, nr.QuantConfig(mode=prec), params)
+    ref = oracle.decode(blocks, bg, cfg)
+    plan = nr.Plan(bg, 46, cfg)
+    x = torch.from_numpy(np.ascontiguousarray(blocks)).cuda()
+
+    def check(out):
+        torch.cuda.synchronize()
+        bits = nr.unpack_bits(out["bits"].cpu().numpy(), plan.k)
+        assert np.array_equal(bits, ref["bits"])
+        assert np.array_equal(out["iters"].cpu().numpy(), ref["iterations"])
+
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    outs = [plan.alloc_outputs(len(blocks)) for _ in range(2)]
+    for _ in range(3):
+        for s, o in zip(streams, outs):
+            s.wait_stream(torch.cuda.current_stream())
+            plan.decode_device(x, o, stream=s.cuda_stream)
+    for o in outs:
+        check(o)
+
+    out = plan.alloc_outputs(len(blocks))
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        plan.decode_device(x, out, stream=s.cuda_stream)  # warm-up outside capture
+        torch.cuda.synchronize()
+        for v in out.values():
+            v.zero_()
+        with torch.cuda.graph(g, stream=s):
+            plan.decode_device(x, out, stream=s.cuda_stream)
+    g.replay()
+    check(out)
+    for v in out.values():
+        v.zero_()
+    g.replay()
+    check(out)
