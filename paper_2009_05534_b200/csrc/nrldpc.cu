@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <bitset>
@@ -395,6 +396,133 @@ __device__ __forceinline__ void process_rows2(const KParams& p, uint32_t tba, ui
   b.scatter(Lg, mreg, k.one, st_ok);
 }
 
+// ---- TM layout (BG1 register-row pairs, Z in 288..384) --------------------
+// L holds the biased half2 itself, 4 bytes per position ({1152+v_a,
+// 1152+v_b}; the low byte of each half is the biased byte u = v + 128), so
+// the gather needs no unpack and the scatter no pack. That doubles L
+// (104 KB at Z=384), so the messages leave shared memory: rows with w >= 7
+// keep one biased half2 per edge in shared memory (thread-major, odd word
+// stride), rows with w <= 6 in tensor memory (tcgen05.ld/st, 32x32b: the
+// thread's own TMEM lane; 3 warps share a lane quarter, each owning a
+// 170-column slot). Rows 0..5 keep their byte-pair register messages. The
+// message kind follows from the compile-time row weight (host: tm_layout).
+template <int MAXW, bool REGMSG>
+struct RowWorkTM {
+  static constexpr bool TMEM = !REGMSG && MAXW <= 6;
+  uint32_t off[MAXW];
+  half2 t[MAXW];
+  uint32_t mw[MAXW];  // the row's messages (shared / tensor memory kinds)
+  half2 m1, m2;
+  uint32_t S;
+  uint32_t Ma;  // shared address (w >= 7) or tensor-memory address (w <= 6) of the row's messages
+
+  // thread-private part (tables, addresses, own messages): may run before the
+  // barrier that closes the previous layer
+  __device__ __forceinline__ void gather_pro(const KParams& p, uint32_t tb, uint32_t mb, uint32_t zl, uint32_t ZL,
+                                             uint32_t Mzs, uint32_t tbase) {
+    uint32_t tsh[MAXW], tcb[MAXW];
+    load_row_tables<MAXW>(p, tb, MAXW, tsh, tcb);
+    if constexpr (TMEM) {
+      Ma = tbase + mb;
+      tm_ld_row<MAXW>(Ma, mw);
+    } else if constexpr (!REGMSG) {
+      Ma = Mzs + mb;
+#pragma unroll
+      for (int j = 0; j < MAXW; ++j) mw[j] = lds_u32(Ma + 4 * j);
+    }
+#pragma unroll
+    for (int j = 0; j < MAXW; ++j) off[j] = edge_offset(tsh[j], tcb[j], zl, ZL);
+  }
+  __device__ __forceinline__ void gather_main(const uint32_t* mreg, uint32_t magic) {
+    if constexpr (TMEM) tm_wait_ld<MAXW>(mw);
+    S = 0;
+#pragma unroll
+    for (int j = 0; j < MAXW; ++j) {
+      const half2 lh = u2h(lds_u32(off[j]));
+      const half2 mh = REGMSG ? msg_load<2, true>(nullptr, 0, mreg, j, j, magic) : u2h(mw[j]);
+      const half2 tj = __hsub2(lh, mh);  // exact: L - M
+      S ^= h2u(tj);
+      t[j] = tj;
+    }
+    two_smallest<MAXW>(t, m1, m2);  // kernels.py:247-250
+  }
+  half2 dd, b2s;
+  __device__ __forceinline__ void beta_arith(const Consts& k) {
+    const half2 sig = u2h((S & 0x80008000u) | k.one);
+    const half2 bh = u2h(k.bh), nd = u2h(k.nd), cc = u2h(k.cc);
+    const half2 B1 = __hfma2(__hadd2(m1, nd), bh, cc);
+    const half2 B2 = __hfma2(__hadd2(m2, nd), bh, cc);
+    dd = __hmul2(__hsub2(B1, B2), sig);
+    b2s = __hmul2(__hsub2(B2, cc), sig);
+  }
+  __device__ __forceinline__ void scatter(uint32_t* mreg, uint32_t one) {
+    const half2 H127 = u2h(0x57F057F0u);   // 127.0
+    const half2 H1152 = u2h(0x64806480u);  // 1152.0
+#pragma unroll
+    for (int j = 0; j < MAXW; ++j) {
+      const half2 x = __hsub2_sat(__habs2(t[j]), m1);
+      const half2 mag = __hfma2(x, dd, b2s);
+      const half2 a = __hmin2(__habs2(t[j]), H127);
+      const half2 y = __hmin2(__hadd2(a, mag), H127);
+      const half2 sg = u2h((h2u(t[j]) & 0x80008000u) | one);
+      sts_u32(off[j], h2u(__hfma2(y, sg, H1152)));
+      const half2 mb = __hfma2(mag, sg, H1152);
+      if constexpr (REGMSG) msg_store<2, true>(nullptr, 0, mreg, j, j, mb, true);
+      else if constexpr (TMEM) mw[j] = h2u(mb);
+      else sts_u32(Ma + 4 * j, h2u(mb));
+    }
+    if constexpr (TMEM) tm_st_row<MAXW>(Ma, mw);
+  }
+};
+
+struct TmCtx {
+  uint32_t zl, ZL;
+  uint32_t Ms;     // shared-window address of this thread's message row
+  uint32_t tbase;  // tensor-memory address of this thread's column slot
+  Consts k;
+};
+
+template <int W, bool REGMSG>
+__device__ __forceinline__ void process_row_tm(const KParams& p, uint32_t tb, uint32_t mb, const TmCtx& c,
+                                               uint32_t* mreg, bool bar) {
+  RowWorkTM<W, REGMSG> r;
+  r.gather_pro(p, tb, mb, c.zl, c.ZL, c.Ms, c.tbase);
+  if (bar) __syncthreads();
+  r.gather_main(mreg, c.k.magic);
+  r.beta_arith(c.k);
+  r.scatter(mreg, c.k.one);
+}
+
+template <int WA, int WB>
+__device__ __forceinline__ void process_rows2_tm(const KParams& p, uint32_t tba, uint32_t mba, uint32_t tbb,
+                                                 uint32_t mbb, const TmCtx& c, bool bar) {
+  RowWorkTM<WA, false> a;
+  RowWorkTM<WB, false> b;
+  a.gather_pro(p, tba, mba, c.zl, c.ZL, c.Ms, c.tbase);
+  b.gather_pro(p, tbb, mbb, c.zl, c.ZL, c.Ms, c.tbase);
+  if (bar) __syncthreads();
+  a.gather_main(nullptr, c.k.magic);
+  b.gather_main(nullptr, c.k.magic);
+  a.beta_arith(c.k);
+  b.beta_arith(c.k);
+  a.scatter(nullptr, c.k.one);
+  b.scatter(nullptr, c.k.one);
+}
+
+template <int MAXW>
+__device__ __forceinline__ void row_parity_tm(const KParams& p, const uint32_t tb, uint32_t zl, uint32_t ZL,
+                                              int& wa, int& wb) {
+  uint32_t tsh[MAXW], tcb[MAXW];
+  load_row_tables<MAXW>(p, tb, MAXW, tsh, tcb);
+  uint32_t x = 0;
+#pragma unroll
+  for (int j = 0; j < MAXW; ++j) x ^= lds_u32(edge_offset(tsh[j], tcb[j], zl, ZL));
+  // bit 7 of each half's low byte is 1 for a non-negative value
+  if (MAXW & 1) x ^= 0x00800080u;
+  wa += (x >> 7) & 1u;
+  wb += (x >> 23) & 1u;
+}
+
 // Syndrome weight (decoder.py:323-329) and min|L| (decoder.py:480-483) over
 // the thread's check rows / columns.
 template <int MAXW, int LANES, bool ABS = false>
@@ -646,6 +774,69 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
   }
 }
 
+// one_iteration for the TM layout (BG1, NREG == 6): same schedule, units and
+// barrier placement
+__device__ __forceinline__ void one_iteration_tm(const KParams& p, const TmCtx& c, RegMsg<6>& rm) {
+#pragma unroll 1
+  for (int r = 0; r < 4; r += 2) {
+    process_row_tm<19, true>(p, 5u * r, 0, c, rm.q[0], r != 0);
+    process_row_tm<19, true>(p, 5u * r + 5u, 0, c, rm.q[1], true);
+    rm.rotate2();
+  }
+  process_row_tm<3, true>(p, 20u, 0, c, rm.r4, true);
+  process_row_tm<8, true>(p, 21u, 0, c, rm.r5, true);
+  bool bar_prev = true;
+  uint32_t ncode = p.unit_a[0].x;
+#pragma unroll 1
+  for (int u = 0; u < p.n_units; ++u) {
+    const uint32_t code = ncode;
+    const uint4 A = p.unit_a[u];
+    const uint4 B = p.unit_b[u];
+    ncode = p.unit_a[u + 1].x;
+    dispatch_unit<1, 6>(code, [&](auto WA, auto WB) {
+      constexpr int wa = decltype(WA)::value, wb = decltype(WB)::value;
+      if constexpr (wb == 0) process_row_tm<wa, false>(p, A.z, A.w, c, nullptr, bar_prev);
+      else process_rows2_tm<wa, wb>(p, A.z, A.w, B.x, B.y, c, bar_prev);
+    });
+    bar_prev = A.y != 0;
+  }
+  if (bar_prev) __syncthreads();
+  // the next iteration reads these messages back
+  tm_wait_st();
+}
+
+// local_check for the TM layout (Z % 32 == 0, one group)
+__device__ __forceinline__ void local_check_tm(const KParams& p, uint32_t zl, uint32_t ZL, uint32_t Ls, int* wcnt,
+                                               int* mabs, bool early, bool need_a, bool need_b) {
+  int wa = 0, wb = 0;
+  bool stopped = false;
+#pragma unroll 1
+  for (int r = 0; r < p.rows; ++r) {
+    const int e0 = p.row_start[r];
+    const int t0 = p.tab_start[r];
+    const int w = p.row_start[r + 1] - e0;
+    dispatch_w<1>(w, [&](auto W) { row_parity_tm<decltype(W)::value>(p, t0 / 4u, zl, ZL, wa, wb); });
+    if (early) {
+      const bool fa = !need_a || __any_sync(0xFFFFFFFFu, wa != 0);
+      const bool fb = !need_b || __any_sync(0xFFFFFFFFu, wb != 0);
+      if (fa && fb) {
+        stopped = true;
+        break;
+      }
+    }
+  }
+  int ma = 255, mb = 255;
+  for (int c = 0; c < p.n_blocks && !stopped; ++c) {
+    const uint32_t u = lds_u32(Ls + (uint32_t)c * ZL + zl);
+    ma = min(ma, abs((int)(u & 0xFFu) - 128));
+    mb = min(mb, abs((int)((u >> 16) & 0xFFu) - 128));
+  }
+  wcnt[0] = wa;
+  wcnt[1] = wb;
+  mabs[0] = ma;
+  mabs[1] = mb;
+}
+
 // early: only "any unsatisfied check" matters (an early-stop iteration that
 // is neither traced nor the last). A warp then stops scanning rows once it
 // holds a failing check of every lane still being decoded (need_a/need_b):
@@ -715,7 +906,7 @@ __device__ __forceinline__ void write_bits(const KParams& p, const uint8_t* __re
 // The same with whole warps when Z % 32 == 0 (warps never straddle groups):
 // lane t of a warp reads position 32*w + t of both codewords with one
 // coalesced load and two ballots build the two packed words.
-template <int LANES>
+template <int LANES, uint32_t ES = LANES>
 __device__ __forceinline__ void write_bits_warp(const KParams& p, const uint8_t* __restrict__ Lg, int z,
                                                 const int (&need)[2], long long cw0,
                                                 uint32_t* __restrict__ bits, long long cw1 = -1) {
@@ -724,9 +915,12 @@ __device__ __forceinline__ void write_bits_warp(const KParams& p, const uint8_t*
   const int lid = z & 31;
   for (int wi = z >> 5; wi < p.words; wi += p.z >> 5) {
     const int pos = wi * 32 + lid;
-    const uint32_t u = pos < K ? ld_elem<LANES>(Lg + pos * LANES) : 0x8080u;
+    // lane b's byte: byte 1 (byte pairs) or byte 2 (TM half2)
+    constexpr int sb = ES == 4 ? 16 : 8;
+    const uint32_t u = pos < K ? (ES == 4 ? *reinterpret_cast<const uint32_t*>(Lg + pos * 4) : ld_elem<LANES>(Lg + pos * LANES))
+                               : (0x80u | (0x80u << sb));
     const uint32_t wa = __ballot_sync(0xFFFFFFFFu, (u & 0xFFu) < 128u);
-    const uint32_t wb = __ballot_sync(0xFFFFFFFFu, ((u >> 8) & 0xFFu) < 128u);
+    const uint32_t wb = __ballot_sync(0xFFFFFFFFu, ((u >> sb) & 0xFFu) < 128u);
     if (lid == 0) {
       if (need[0]) bits[cw0 * p.words + wi] = wa;
       if (LANES == 2 && need[1]) bits[cw1 * p.words + wi] = wb;
@@ -739,13 +933,13 @@ __device__ __forceinline__ void write_bits_warp(const KParams& p, const uint8_t*
 // XOR over set bits i of rem(x^(K-1-i+L), g), tabulated on the host
 // (crc_tab[i]). Each thread folds positions i = z, z+Z, ... and XORs its
 // partial into the group's accumulator; the check passes when the XOR is 0.
-template <int LANES>
+template <int LANES, uint32_t ES = LANES>
 __device__ __forceinline__ uint32_t crc_partial(const KParams& p, const uint8_t* __restrict__ Lg, int z,
                                                 int lane) {
   const int K = p.k_b * p.z;
   uint32_t acc = 0;
   for (int i = z; i < K; i += p.z) {
-    const uint32_t neg = Lg[i * LANES + lane] < 128u ? 0xFFFFFFFFu : 0u;
+    const uint32_t neg = Lg[i * ES + (ES == 4 ? 2 : 1) * lane] < 128u ? 0xFFFFFFFFu : 0u;
     acc ^= __ldg(p.crc_tab + i) & neg;
   }
   return acc;
@@ -756,11 +950,13 @@ __device__ __forceinline__ uint32_t crc_partial(const KParams& p, const uint8_t*
 // Threads beyond G*Z (warp padding) shadow the last group's z = tid - (G-1)*Z
 // clamp but never store, so the layer loop runs warp-uniform and the graph
 // tables stay in uniform registers.
-template <int BG, int MAXW, int LANES, int NREG, bool ABS>
+template <int BG, int MAXW, int LANES, int NREG, bool ABS, bool TM = false>
 __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_constant__ KParams p,
                                                                    const int8_t* __restrict__ llr, KOut o) {
   static_assert(NREG == 0 || (BG == 1 && LANES == 2), "register messages: BG1 pairs only");
   static_assert(!ABS || BG != 0, "absolute addressing: compile-time schedules only");
+  static_assert(!TM || (BG == 1 && LANES == 2 && NREG == 6 && ABS), "TM layout: BG1 register-row pairs");
+  constexpr uint32_t ES = TM ? 4 : LANES;  // bytes per position of L
   extern __shared__ __align__(16) uint8_t smem[];
   uint16_t* lut = reinterpret_cast<uint16_t*>(smem);
   CtaState* cta = reinterpret_cast<CtaState*>(smem + kLutBytes);
@@ -775,8 +971,8 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
   const int z = st_ok ? tid - g * p.z : (tid - g * p.z) % p.z;
   const long long cw0 = ((long long)blockIdx.x * p.groups + g) * LANES;
   const bool active = st_ok && cw0 < p.batch;        // owns real codewords
-  const uint32_t ZL = (uint32_t)p.z * LANES;
-  const uint32_t zl = (uint32_t)z * LANES;
+  const uint32_t ZL = (uint32_t)p.z * ES;
+  const uint32_t zl = (uint32_t)z * ES;
   const long long n_c = (long long)p.n_blocks * p.z;
   uint8_t* Lg = smem + data_off + (uint32_t)g * (p.l_bytes + p.m_bytes);
   uint8_t* Mz = Lg + p.l_bytes + (uint32_t)z * p.m_stride;
@@ -807,6 +1003,21 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
       gs.done[l] = 0;
       gs.accept[l] = 0;
     }
+  }
+
+  uint32_t tbase = 0;  // TM: this thread's tensor-memory column slot
+  if constexpr (TM) {
+    if (tid < 32) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(&cta->kc[5])));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const int warp = tid >> 5;
+    // 3 warps per lane quarter, 170 columns each (host: tm_layout)
+    tbase = lds_u32(&cta->kc[5]) + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * 170u;
   }
 
   bool lane_valid[2];
@@ -849,11 +1060,25 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
             bad |= (b.x - 0x01010101u) & ~b.x; bad |= (b.y - 0x01010101u) & ~b.y;
             bad |= (b.z - 0x01010101u) & ~b.z; bad |= (b.w - 0x01010101u) & ~b.w;
           }
+          if constexpr (TM) {
+            // position i of the chunk -> {0x64, u_b, 0x64, u_a} (biased half2)
+            uint4* dst = reinterpret_cast<uint4*>(Lg) + 4 * k;
+            const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint32_t w4[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                w4[i] = (__byte_perm(av[q], bv[q], 0x0400u + 0x0101u * i) & 0x00FF00FFu) | 0x64006400u;
+              dst[q] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+            }
+          } else {
           uint4* dst = reinterpret_cast<uint4*>(Lg) + 2 * k;
           dst[0] = make_uint4(__byte_perm(a.x, b.x, 0x5140), __byte_perm(a.x, b.x, 0x7362),
                               __byte_perm(a.y, b.y, 0x5140), __byte_perm(a.y, b.y, 0x7362));
           dst[1] = make_uint4(__byte_perm(a.z, b.z, 0x5140), __byte_perm(a.z, b.z, 0x7362),
                               __byte_perm(a.w, b.w, 0x5140), __byte_perm(a.w, b.w, 0x7362));
+          }
         } else {
           reinterpret_cast<uint4*>(Lg)[k] = a;
         }
@@ -874,12 +1099,26 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
           }
           v |= u << (8 * l);
         }
-        st_elem<LANES>(Lg + (uint32_t)n * LANES, v);
+        if constexpr (TM)
+          *reinterpret_cast<uint32_t*>(Lg + (uint32_t)n * 4) = (v & 0xFFu) | ((v & 0xFF00u) << 8) | 0x64006400u;
+        else
+          st_elem<LANES>(Lg + (uint32_t)n * LANES, v);
       }
     }
     // messages: the group's whole message area is contiguous (m_bytes % 16 == 0)
     uint4* m4 = reinterpret_cast<uint4*>(Lg + p.l_bytes);
+    if constexpr (TM) {
+      // biased zero half2 (1152.0) in shared and tensor memory
+      const uint4 hz = make_uint4(0x64806480u, 0x64806480u, 0x64806480u, 0x64806480u);
+      for (uint32_t k = z; k < (p.m_bytes >> 4); k += p.z) m4[k] = hz;
+      const uint32_t h = 0x64806480u;
+      uint32_t c = 0;
+      for (; c + 4 <= p.tm_cols; c += 4) tm_st4(tbase + c, h, h, h, h);
+      for (; c < p.tm_cols; ++c) tm_st1(tbase + c, h);
+      tm_wait_st();
+    } else {
     for (uint32_t k = z; k < (p.m_bytes >> 4); k += p.z) m4[k] = zero4;
+    }
     if (bad && o.status) atomicOr(o.status, 1);
   }
   __syncthreads();
@@ -887,10 +1126,12 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
   const Consts kc{lds_u32(&cta->kc[0]), lds_u32(&cta->kc[1]), lds_u32(&cta->kc[2]), lds_u32(&cta->kc[3]),
                   lds_u32(&cta->kc[4])};
   const RowCtx rc{zl, ZL, Lg, Mz, (uint32_t)__cvta_generic_to_shared(Mz), lut, kc, st_ok};
+  const TmCtx tc{zl, ZL, (uint32_t)__cvta_generic_to_shared(Mz), tbase, kc};
   RegMsg<NREG> rm;
   rm.init();
   for (int it = 1; it <= p.max_iter; ++it) {
-    one_iteration<BG, MAXW, LANES, NREG, ABS>(p, rc, rm);
+    if constexpr (TM) one_iteration_tm(p, tc, rm);
+    else one_iteration<BG, MAXW, LANES, NREG, ABS>(p, rc, rm);
     const bool last = it == p.max_iter;
     if (!(p.early_stop != NRLDPC_STOP_NONE || p.trace || last)) continue;
 
@@ -899,8 +1140,12 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
       int wc[2], ma[2];
       // weights are only needed in full when traced or final
       const bool early = BG != 0 && !p.trace && !last && p.z % 32 == 0;
-      local_check<BG, MAXW, LANES, ABS>(p, zl, ZL, Lg, wc, ma, early, lane_valid[0] && !gs.done[0],
-                                        lane_valid[1] && !gs.done[1]);
+      if constexpr (TM)
+        local_check_tm(p, zl, ZL, p.abs_base, wc, ma, early, lane_valid[0] && !gs.done[0],
+                       lane_valid[1] && !gs.done[1]);
+      else
+        local_check<BG, MAXW, LANES, ABS>(p, zl, ZL, Lg, wc, ma, early, lane_valid[0] && !gs.done[0],
+                                          lane_valid[1] && !gs.done[1]);
       if (active) {
 #pragma unroll
         for (int l = 0; l < LANES; ++l) {
@@ -921,7 +1166,7 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
 #pragma unroll
         for (int l = 0; l < LANES; ++l) {
           if (cand[l]) {
-            const uint32_t part = p.crc_tab ? crc_partial<LANES>(p, Lg, z, l) : 1u;
+            const uint32_t part = p.crc_tab ? crc_partial<LANES, ES>(p, Lg, z, l) : 1u;
             if (part) atomicXor(reinterpret_cast<unsigned int*>(&gs.accept[l]), part);
           }
         }
@@ -939,7 +1184,7 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
       const int need[2] = {cand[0] || fin[0], LANES == 2 && (cand[1] || fin[1])};
       if (p.z % 32 == 0) {
         // group-uniform condition, whole warps per group: ballots are safe
-        if (need[0] || need[1]) write_bits_warp<LANES>(p, Lg, z, need, cw0, o.bits);
+        if (need[0] || need[1]) write_bits_warp<LANES, ES>(p, Lg, z, need, cw0, o.bits);
       } else {
 #pragma unroll
         for (int l = 0; l < LANES; ++l)
@@ -989,6 +1234,12 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
     // block-wide vote: provably uniform, so the layer loop stays on the
     // uniform datapath (graph tables in uniform registers)
     if (__syncthreads_and(!p.trace && cta->n_done >= cta->n_valid)) break;
+  }
+  if constexpr (TM) {
+    tm_wait_st();
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(lds_u32(&cta->kc[5])));
   }
 }
 
@@ -1379,7 +1630,9 @@ struct Shape {
   size_t smem = 0;
   int occ = 0;      // resident CTAs per SM (0: not queried yet)
   bool abs = false; // kp.cb holds absolute shared-window addresses
+  bool tm = false;  // TM layout (half2 L, shared/tensor-memory messages)
   KParams kp{};
+  std::shared_ptr<Shape> alt;  // TM shapes: the byte-pair shape (lane-refill kernel)
 };
 
 struct nrldpc_plan {
@@ -1442,11 +1695,11 @@ size_t smem_for(int groups, size_t l_bytes, size_t m_bytes) {
 
 // Launch (or, with llr == nullptr, only prepare: set the smem attribute and
 // query occupancy) one decode kernel instance for `sh`.
-template <int BG, int MAXW, int LANES, int NREG = 0, bool ABS = false>
+template <int BG, int MAXW, int LANES, int NREG = 0, bool ABS = false, bool TM = false>
 cudaError_t launch_i8(Shape& sh, int device, const int8_t* llr, long long batch, const KOut& o,
                       cudaStream_t st) {
   static bool attr_done[64] = {};
-  auto kern = k_decode_i8<BG, MAXW, LANES, NREG, ABS>;
+  auto kern = k_decode_i8<BG, MAXW, LANES, NREG, ABS, TM>;
   if (!attr_done[device & 63]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (e != cudaSuccess) return e;
@@ -1747,6 +2000,51 @@ Shape choose_shape(const nrldpc_plan* p, int max_lanes) {
   return sh;
 }
 
+// TM layout of a register-row shape (k_decode_i8 TM): L as biased half2,
+// messages of rows >= 6 with w >= 7 in shared memory (one half2 per edge,
+// odd word stride) and w <= 6 in tensor memory (one column per edge, at most
+// 170 columns per thread). Returns the byte-pair shape unchanged when the
+// layout does not fit; NRLDPC_NO_TM=1 disables it.
+constexpr uint32_t kTmColsPerThread = 170;
+Shape tm_shape(const nrldpc_plan* p, const Shape& leg) {
+  if (leg.nreg != 6 || !leg.abs || leg.groups != 1 || p->z % 32 != 0 || p->z > 384 || getenv("NRLDPC_NO_TM"))
+    return leg;
+  const size_t smem_max = 232448;
+  const KParams& b = p->base;
+  MsgLayout ml{};
+  uint32_t sm_slots = 0, tm_cols = 0;
+  for (int r = 6; r < p->rows; ++r) {
+    const int w = b.row_start[r + 1] - b.row_start[r];
+    if (w >= 7) {
+      ml.mb[r] = sm_slots * 4u;
+      sm_slots += (uint32_t)w;
+    } else {
+      ml.mb[r] = tm_cols;
+      tm_cols += (uint32_t)w;
+    }
+  }
+  if (tm_cols > kTmColsPerThread) return leg;
+  uint32_t e = sm_slots | 1u;  // odd word stride: conflict-free across z
+  const size_t lb = align16((size_t)p->n_blocks * p->z * 4);
+  const size_t mb = align16((size_t)p->z * e * 4);
+  if (smem_for(1, lb, mb) > smem_max) return leg;
+  Shape sh = leg;
+  sh.tm = true;
+  sh.occ = 0;
+  sh.smem = smem_for(1, lb, mb);
+  sh.kp.l_bytes = (uint32_t)lb;
+  sh.kp.m_bytes = (uint32_t)mb;
+  sh.kp.m_stride = e * 4u;
+  sh.kp.tm_cols = tm_cols;
+  build_units(p, 6, ml, sh.kp);
+  for (int t = 0; t < NR_MAX_TAB; ++t) {
+    sh.kp.sh[t] = b.sh[t] * 4u;
+    sh.kp.cb[t] = b.cb[t] * (uint32_t)p->z * 4u + sh.kp.abs_base;
+  }
+  sh.alt = std::make_shared<Shape>(leg);
+  return sh;
+}
+
 }  // namespace
 
 // Persistent lane-refill launch (early-stop modes, single-group pair shapes):
@@ -1794,18 +2092,21 @@ static cudaError_t launch_shape(const nrldpc_plan* plan, Shape& sh, const int8_t
   if (sh.threads == 0) return cudaErrorInvalidConfiguration;  // no feasible shape
   const bool two = sh.lanes == 2;
   const int dev = plan->device;
-  // early-stop modes without a trace: refill lanes as codewords stop
-  const bool refill = plan->early_stop != NRLDPC_STOP_NONE && o.trace_w == nullptr && sh.abs && two &&
-                      sh.groups == 1 && plan->z % 32 == 0 && !getenv("NRLDPC_NO_REFILL");
+  // early-stop modes without a trace: refill lanes as codewords stop (the
+  // refill kernel runs the byte-pair layout: a TM shape carries it in alt)
+  Shape& rs = sh.alt ? *sh.alt : sh;
+  const bool refill = plan->early_stop != NRLDPC_STOP_NONE && o.trace_w == nullptr && rs.abs && two &&
+                      rs.groups == 1 && plan->z % 32 == 0 && !getenv("NRLDPC_NO_REFILL");
   if (refill && (in == nullptr || batch > 2)) {
     cudaError_t e = cudaSuccess;
-    if (plan->schedule == 1 && sh.nreg == 6) e = launch_refill<1, 19, 6>(sh, dev, in, batch, o, st);
-    else if (plan->schedule == 1 && sh.nreg == 0) e = launch_refill<1, 19, 0>(sh, dev, in, batch, o, st);
-    else if (plan->schedule == 2 && sh.nreg == 0) e = launch_refill<2, 10, 0>(sh, dev, in, batch, o, st);
+    if (plan->schedule == 1 && rs.nreg == 6) e = launch_refill<1, 19, 6>(rs, dev, in, batch, o, st);
+    else if (plan->schedule == 1 && rs.nreg == 0) e = launch_refill<1, 19, 0>(rs, dev, in, batch, o, st);
+    else if (plan->schedule == 2 && rs.nreg == 0) e = launch_refill<2, 10, 0>(rs, dev, in, batch, o, st);
     else goto plain;
     if (in != nullptr || e != cudaSuccess) return e;
   }
 plain:
+  if (sh.tm) return launch_i8<1, 19, 2, 6, true, true>(sh, dev, in, batch, o, st);
   switch (plan->schedule) {
     case 1:
       if (!two) return launch_i8<1, 19, 1>(sh, dev, in, batch, o, st);
@@ -2226,6 +2527,7 @@ int nrldpc_plan_create(int device, int k_b, int z, int rows_used, const int32_t*
   const char* force = std::getenv("NRLDPC_FORCE_LANES");
   if (precision == NRLDPC_INT8) {
     p->main = choose_shape(p, force && force[0] == '1' ? 1 : 2);
+    p->main = tm_shape(p, p->main);
   } else {
     p->main = choose_shape_float(p);
     if (p->schedule != 0) {
@@ -2270,7 +2572,7 @@ int nrldpc_plan_set_coscheduled(nrldpc_plan* plan, int on) {
   if (plan->precision != NRLDPC_INT8 || plan->coscheduled == (on != 0)) return NRLDPC_OK;
   plan->coscheduled = on != 0;
   const char* force = std::getenv("NRLDPC_FORCE_LANES");
-  Shape sh = choose_shape(plan, force && force[0] == '1' ? 1 : 2);
+  Shape sh = tm_shape(plan, choose_shape(plan, force && force[0] == '1' ? 1 : 2));
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(plan->device);

@@ -55,6 +55,7 @@ struct alignas(16) KParams {
   uint32_t magic;    // 0x64646464: PRMT filler byte (half exponent of 1024)
   uint32_t one;      // 0x3C003C00: half2 {1.0, 1.0}
   uint32_t abs_base; // nonzero: cb holds shared-window addresses, L starts here
+  uint32_t tm_cols;  // TM layout: tensor-memory message columns per thread
   uint16_t row_start[NR_MAX_ROWS + 1];  // first edge of each row (message offsets)
   uint16_t tab_start[NR_MAX_ROWS + 1];  // row's first slot in sh/cb (multiple of 4)
   uint8_t bar_after[NR_MAX_ROWS];       // 0: next row is column-disjoint from this layer
@@ -172,6 +173,66 @@ __device__ __forceinline__ void sts_u32_if(uint32_t a, uint32_t v, bool ok) {
   asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.u32 [%0], %1; }" ::"r"(a), "r"(v),
                "r"((uint32_t)ok));
 }
+
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v));
+}
+
+// Tensor memory as per-thread message storage (TM layout, see k_decode_i8).
+// tcgen05.ld / tcgen05.st with the 32x32b shape move N consecutive 32-bit
+// columns of the executing thread's own TMEM lane; the address is warp-uniform
+// (lane quarter in bits 31:16, column in bits 15:0) and the instructions are
+// warp-collective. A row of W messages is one x4 plus an x2 / x1 remainder.
+__device__ __forceinline__ void tm_ld1(uint32_t a, uint32_t& r0) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r0) : "r"(a));
+}
+__device__ __forceinline__ void tm_ld2(uint32_t a, uint32_t& r0, uint32_t& r1) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(a));
+}
+__device__ __forceinline__ void tm_ld4(uint32_t a, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(a));
+}
+__device__ __forceinline__ void tm_st1(uint32_t a, uint32_t r0) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(a), "r"(r0));
+}
+__device__ __forceinline__ void tm_st2(uint32_t a, uint32_t r0, uint32_t r1) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(a), "r"(r0), "r"(r1));
+}
+__device__ __forceinline__ void tm_st4(uint32_t a, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(r0), "r"(r1),
+               "r"(r2), "r"(r3));
+}
+
+template <int W>
+__device__ __forceinline__ void tm_ld_row(uint32_t a, uint32_t (&r)[W]) {
+#pragma unroll
+  for (int k = 0; k + 4 <= W; k += 4) tm_ld4(a + k, r[k], r[k + 1], r[k + 2], r[k + 3]);
+  constexpr int k2 = W / 4 * 4;
+  if constexpr ((W & 2) != 0) tm_ld2(a + k2, r[k2], r[k2 + 1]);
+  if constexpr ((W & 1) != 0) tm_ld1(a + W - 1, r[W - 1]);
+}
+
+template <int W>
+__device__ __forceinline__ void tm_st_row(uint32_t a, const uint32_t (&r)[W]) {
+#pragma unroll
+  for (int k = 0; k + 4 <= W; k += 4) tm_st4(a + k, r[k], r[k + 1], r[k + 2], r[k + 3]);
+  constexpr int k2 = W / 4 * 4;
+  if constexpr ((W & 2) != 0) tm_st2(a + k2, r[k2], r[k2 + 1]);
+  if constexpr ((W & 1) != 0) tm_st1(a + W - 1, r[W - 1]);
+}
+
+// Waits for this thread's outstanding tcgen05.ld; the empty "+r" statements
+// after it make every later use of r depend on the wait.
+template <int W>
+__device__ __forceinline__ void tm_wait_ld(uint32_t (&r)[W]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+  for (int j = 0; j < W; ++j) asm volatile("" : "+r"(r[j]));
+}
+
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;"); }
 
 // beta LUT on a half2 of integer magnitudes 0..127
 __device__ __forceinline__ half2 beta_lut2(const uint16_t* lut, half2 m) {
