@@ -14,7 +14,6 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <memory>
 #include <mutex>
 #include <string>
 #include <bitset>
@@ -1259,11 +1258,13 @@ struct LaneState {
   int pad[2];
 };
 
-template <int BG, int MAXW, int NREG>
+template <int BG, int MAXW, int NREG, bool TM = false>
 __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const __grid_constant__ KParams p,
                                                                           const int8_t* __restrict__ llr, KOut o) {
   constexpr int LANES = 2;
   constexpr bool ABS = true;
+  static_assert(!TM || (BG == 1 && NREG == 6), "TM layout: BG1 register-row pairs");
+  constexpr uint32_t ES = TM ? 4 : LANES;  // bytes per position of L
   extern __shared__ __align__(16) uint8_t smem[];
   LaneState* ls = reinterpret_cast<LaneState*>(smem);  // the (unused) beta-table area
   CtaState* cta = reinterpret_cast<CtaState*>(smem + kLutBytes);
@@ -1272,8 +1273,8 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const 
   const int tid = threadIdx.x;
   const int z = tid;
   const bool st_ok = true;
-  const uint32_t ZL = (uint32_t)p.z * LANES;
-  const uint32_t zl = (uint32_t)z * LANES;
+  const uint32_t ZL = (uint32_t)p.z * ES;
+  const uint32_t zl = (uint32_t)z * ES;
   const long long n_c = (long long)p.n_blocks * p.z;
   uint8_t* Lg = smem + data_off;
   uint8_t* Mz = Lg + p.l_bytes + (uint32_t)z * p.m_stride;
@@ -1295,11 +1296,31 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const 
       gs.accept[l] = 0;
     }
   }
+  uint32_t tbase = 0;  // TM: this thread's tensor-memory column slot (see k_decode_i8)
+  if constexpr (TM) {
+    if (tid < 32) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(&cta->kc[5])));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const int warp = tid >> 5;
+    tbase = lds_u32(&cta->kc[5]) + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * 170u;
+  }
   // messages: all zero (biased)
   {
     uint4* m4 = reinterpret_cast<uint4*>(Lg + p.l_bytes);
-    const uint4 zero4 = make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);
+    const uint32_t zw = TM ? 0x64806480u : 0x80808080u;
+    const uint4 zero4 = make_uint4(zw, zw, zw, zw);
     for (uint32_t k = z; k < (p.m_bytes >> 4); k += p.z) m4[k] = zero4;
+    if constexpr (TM) {
+      uint32_t c = 0;
+      for (; c + 4 <= p.tm_cols; c += 4) tm_st4(tbase + c, zw, zw, zw, zw);
+      for (; c < p.tm_cols; ++c) tm_st1(tbase + c, zw);
+      tm_wait_st();
+    }
   }
   __syncthreads();
 
@@ -1332,17 +1353,34 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const 
         // spread 4 bytes to the lane's byte of 4 positions: 0x5140 -> lane 0,
         // then shift up by 8 for lane 1
         const uint32_t in4[4] = {a.x, a.y, a.z, a.w};
+        if constexpr (TM) {
+          // position -> the lane's half of its half2 word: {0x64, u}
+          uint4* dh = reinterpret_cast<uint4*>(Lg) + 4 * k;
+          const uint32_t keep_h = l ? 0x0000FFFFu : 0xFFFF0000u;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          uint4 d = dst[2 * k + h];
-          const uint32_t u0 = __byte_perm(in4[2 * h], 0, 0x4140), u1 = __byte_perm(in4[2 * h], 0, 0x4342);
-          const uint32_t u2 = __byte_perm(in4[2 * h + 1], 0, 0x4140), u3 = __byte_perm(in4[2 * h + 1], 0, 0x4342);
-          const int sh = 8 * l;
-          d.x = (d.x & keep) | ((u0 << sh) & ~keep);
-          d.y = (d.y & keep) | ((u1 << sh) & ~keep);
-          d.z = (d.z & keep) | ((u2 << sh) & ~keep);
-          d.w = (d.w & keep) | ((u3 << sh) & ~keep);
-          dst[2 * k + h] = d;
+          for (int q = 0; q < 4; ++q) {
+            uint4 d = dh[q];
+            const uint32_t v0 = __byte_perm(in4[q], 0x64646464u, 0x4040u), v1 = __byte_perm(in4[q], 0x64646464u, 0x4141u);
+            const uint32_t v2 = __byte_perm(in4[q], 0x64646464u, 0x4242u), v3 = __byte_perm(in4[q], 0x64646464u, 0x4343u);
+            d.x = (d.x & keep_h) | (v0 & ~keep_h);
+            d.y = (d.y & keep_h) | (v1 & ~keep_h);
+            d.z = (d.z & keep_h) | (v2 & ~keep_h);
+            d.w = (d.w & keep_h) | (v3 & ~keep_h);
+            dh[q] = d;
+          }
+        } else {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint4 d = dst[2 * k + h];
+            const uint32_t u0 = __byte_perm(in4[2 * h], 0, 0x4140), u1 = __byte_perm(in4[2 * h], 0, 0x4342);
+            const uint32_t u2 = __byte_perm(in4[2 * h + 1], 0, 0x4140), u3 = __byte_perm(in4[2 * h + 1], 0, 0x4342);
+            const int sh = 8 * l;
+            d.x = (d.x & keep) | ((u0 << sh) & ~keep);
+            d.y = (d.y & keep) | ((u1 << sh) & ~keep);
+            d.z = (d.z & keep) | ((u2 << sh) & ~keep);
+            d.w = (d.w & keep) | ((u3 << sh) & ~keep);
+            dst[2 * k + h] = d;
+          }
         }
         }
       }
@@ -1351,7 +1389,8 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const 
       for (long long n = z; n < n_c; n += p.z) {
         const int8_t x = src[n];
         bad |= (x == -128);
-        Lg[n * 2 + l] = (uint8_t)x ^ 0x80u;
+        if constexpr (TM) reinterpret_cast<uint16_t*>(Lg)[n * 2 + l] = (uint16_t)(0x6400u | ((uint8_t)x ^ 0x80u));
+        else Lg[n * 2 + l] = (uint8_t)x ^ 0x80u;
       }
     }
     if (bad && o.status) atomicOr(o.status, 1);
@@ -1359,6 +1398,7 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const 
   long long cw[2] = {ls->cw[0], ls->cw[1]};
   for (int l = 0; l < 2; ++l) {
     if (cw[l] >= 0) load_lane(l, cw[l]);
+    else if constexpr (TM) for (long long n = z; n < n_c; n += p.z) reinterpret_cast<uint16_t*>(Lg)[n * 2 + l] = 0x6480u;
     else for (long long n = z; n < n_c; n += p.z) Lg[n * 2 + l] = 0x80u;
   }
   __syncthreads();
@@ -1366,11 +1406,13 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const 
   const Consts kc{lds_u32(&cta->kc[0]), lds_u32(&cta->kc[1]), lds_u32(&cta->kc[2]), lds_u32(&cta->kc[3]),
                   lds_u32(&cta->kc[4])};
   const RowCtx rc{zl, ZL, Lg, Mz, (uint32_t)__cvta_generic_to_shared(Mz), nullptr, kc, st_ok};
+  const TmCtx tc{zl, ZL, (uint32_t)__cvta_generic_to_shared(Mz), tbase, kc};
   RegMsg<NREG> rm;
   rm.init();
   int it[2] = {0, 0};
   while (cw[0] >= 0 || cw[1] >= 0) {
-    one_iteration<BG, MAXW, LANES, NREG, ABS>(p, rc, rm);
+    if constexpr (TM) one_iteration_tm(p, tc, rm);
+    else one_iteration<BG, MAXW, LANES, NREG, ABS>(p, rc, rm);
     bool act[2], last[2];
 #pragma unroll
     for (int l = 0; l < 2; ++l) {
@@ -1380,7 +1422,8 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const 
     }
     {
       int wc[2], ma[2];
-      local_check<BG, MAXW, LANES, ABS>(p, zl, ZL, Lg, wc, ma, !last[0] && !last[1], act[0], act[1]);
+      if constexpr (TM) local_check_tm(p, zl, ZL, p.abs_base, wc, ma, !last[0] && !last[1], act[0], act[1]);
+      else local_check<BG, MAXW, LANES, ABS>(p, zl, ZL, Lg, wc, ma, !last[0] && !last[1], act[0], act[1]);
 #pragma unroll
       for (int l = 0; l < 2; ++l) {
         if (wc[l]) atomicAdd(&gs.synd[l], wc[l]);
@@ -1395,7 +1438,7 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const 
 #pragma unroll
       for (int l = 0; l < 2; ++l) {
         if (cand[l]) {
-          const uint32_t part = p.crc_tab ? crc_partial<LANES>(p, Lg, z, l) : 1u;
+          const uint32_t part = p.crc_tab ? crc_partial<LANES, ES>(p, Lg, z, l) : 1u;
           if (part) atomicXor(reinterpret_cast<unsigned int*>(&gs.accept[l]), part);
         }
       }
@@ -1407,7 +1450,7 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const 
     for (int l = 0; l < 2; ++l) fin[l] = last[l] && !cand[l];
     const int need[2] = {cand[0] || fin[0], cand[1] || fin[1]};
     if (need[0] || need[1]) {
-      write_bits_warp<LANES>(p, Lg, z, need, cw[0], o.bits, cw[1]);
+      write_bits_warp<LANES, ES>(p, Lg, z, need, cw[0], o.bits, cw[1]);
       if (z == 0) {
 #pragma unroll
         for (int l = 0; l < 2; ++l) {
@@ -1441,15 +1484,33 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const 
         if (cw[l] >= 0) {
           load_lane(l, cw[l]);
           // this lane's messages back to zero (bytes l of every 16-bit pair)
-          const uint32_t keep = l ? 0x00FF00FFu : 0xFF00FF00u;
-          const uint32_t zb = 0x80808080u & ~keep;
+          const uint32_t keep = l ? 0x00FF00FFu : 0xFF00FF00u;  // register byte pairs
+          const uint32_t keep_m = TM ? (l ? 0x0000FFFFu : 0xFFFF0000u) : keep;
+          const uint32_t zb = (TM ? 0x64806480u : 0x80808080u) & ~keep_m;
+          if constexpr (TM) {
+            uint32_t c = 0;
+            for (; c + 4 <= p.tm_cols; c += 4) {
+              uint32_t r[4];
+              tm_ld4(tbase + c, r[0], r[1], r[2], r[3]);
+              tm_wait_ld<4>(r);
+              tm_st4(tbase + c, (r[0] & keep_m) | zb, (r[1] & keep_m) | zb, (r[2] & keep_m) | zb,
+                     (r[3] & keep_m) | zb);
+            }
+            for (; c < p.tm_cols; ++c) {
+              uint32_t r[1];
+              tm_ld1(tbase + c, r[0]);
+              tm_wait_ld<1>(r);
+              tm_st1(tbase + c, (r[0] & keep_m) | zb);
+            }
+            tm_wait_st();
+          }
           uint4* m4 = reinterpret_cast<uint4*>(Lg + p.l_bytes);
           for (uint32_t k = z; k < (p.m_bytes >> 4); k += p.z) {
             uint4 v = m4[k];
-            v.x = (v.x & keep) | zb;
-            v.y = (v.y & keep) | zb;
-            v.z = (v.z & keep) | zb;
-            v.w = (v.w & keep) | zb;
+            v.x = (v.x & keep_m) | zb;
+            v.y = (v.y & keep_m) | zb;
+            v.z = (v.z & keep_m) | zb;
+            v.w = (v.w & keep_m) | zb;
             m4[k] = v;
           }
           rm.reset_lane(keep);
@@ -1457,6 +1518,12 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const 
       }
     }
     __syncthreads();
+  }
+  if constexpr (TM) {
+    tm_wait_st();
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(lds_u32(&cta->kc[5])));
   }
 }
 
@@ -1632,7 +1699,6 @@ struct Shape {
   bool abs = false; // kp.cb holds absolute shared-window addresses
   bool tm = false;  // TM layout (half2 L, shared/tensor-memory messages)
   KParams kp{};
-  std::shared_ptr<Shape> alt;  // TM shapes: the byte-pair shape (lane-refill kernel)
 };
 
 struct nrldpc_plan {
@@ -2041,7 +2107,6 @@ Shape tm_shape(const nrldpc_plan* p, const Shape& leg) {
     sh.kp.sh[t] = b.sh[t] * 4u;
     sh.kp.cb[t] = b.cb[t] * (uint32_t)p->z * 4u + sh.kp.abs_base;
   }
-  sh.alt = std::make_shared<Shape>(leg);
   return sh;
 }
 
@@ -2050,12 +2115,12 @@ Shape tm_shape(const nrldpc_plan* p, const Shape& leg) {
 // Persistent lane-refill launch (early-stop modes, single-group pair shapes):
 // one CTA per resident slot, each refilling its lanes from a per-launch
 // codeword counter.
-template <int BG, int MAXW, int NREG>
+template <int BG, int MAXW, int NREG, bool TM = false>
 static cudaError_t launch_refill(Shape& sh, int device, const int8_t* llr, long long batch, const KOut& o,
                                  cudaStream_t st) {
   static bool attr_done[64] = {};
   static int occ_cache[64] = {}, sms[64] = {};
-  auto kern = k_decode_i8_refill<BG, MAXW, NREG>;
+  auto kern = k_decode_i8_refill<BG, MAXW, NREG, TM>;
   const int d = device & 63;
   if (!attr_done[d]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
@@ -2092,16 +2157,15 @@ static cudaError_t launch_shape(const nrldpc_plan* plan, Shape& sh, const int8_t
   if (sh.threads == 0) return cudaErrorInvalidConfiguration;  // no feasible shape
   const bool two = sh.lanes == 2;
   const int dev = plan->device;
-  // early-stop modes without a trace: refill lanes as codewords stop (the
-  // refill kernel runs the byte-pair layout: a TM shape carries it in alt)
-  Shape& rs = sh.alt ? *sh.alt : sh;
-  const bool refill = plan->early_stop != NRLDPC_STOP_NONE && o.trace_w == nullptr && rs.abs && two &&
-                      rs.groups == 1 && plan->z % 32 == 0 && !getenv("NRLDPC_NO_REFILL");
+  // early-stop modes without a trace: refill lanes as codewords stop
+  const bool refill = plan->early_stop != NRLDPC_STOP_NONE && o.trace_w == nullptr && sh.abs && two &&
+                      sh.groups == 1 && plan->z % 32 == 0 && !getenv("NRLDPC_NO_REFILL");
   if (refill && (in == nullptr || batch > 2)) {
     cudaError_t e = cudaSuccess;
-    if (plan->schedule == 1 && rs.nreg == 6) e = launch_refill<1, 19, 6>(rs, dev, in, batch, o, st);
-    else if (plan->schedule == 1 && rs.nreg == 0) e = launch_refill<1, 19, 0>(rs, dev, in, batch, o, st);
-    else if (plan->schedule == 2 && rs.nreg == 0) e = launch_refill<2, 10, 0>(rs, dev, in, batch, o, st);
+    if (sh.tm) e = launch_refill<1, 19, 6, true>(sh, dev, in, batch, o, st);
+    else if (plan->schedule == 1 && sh.nreg == 6) e = launch_refill<1, 19, 6>(sh, dev, in, batch, o, st);
+    else if (plan->schedule == 1 && sh.nreg == 0) e = launch_refill<1, 19, 0>(sh, dev, in, batch, o, st);
+    else if (plan->schedule == 2 && sh.nreg == 0) e = launch_refill<2, 10, 0>(sh, dev, in, batch, o, st);
     else goto plain;
     if (in != nullptr || e != cudaSuccess) return e;
   }

@@ -533,3 +533,42 @@ def test_scratch_paths_capture_and_concurrent_streams(cuda_ok, prec, stop):
         v.zero_()
     g.replay()
     check(out)
+
+
+@pytest.mark.parametrize("z,rows,stop,batch", [(384, 46, "none", 64), (288, 46, "none", 37), (320, 9, "none", 20),
+                                                (352, 46, "syndrome", 2), (384, 30, "crc", 2),
+                                                (384, 6, "none", 8), (384, 7, "none", 8)])
+def test_tm_layout_matches_byte_pair_layout_and_oracle(cuda_ok, z, rows, stop, batch, monkeypatch):
+    """BG1 register-row pairs (Z = 288..384) decode on the TM layout (half2
+    posteriors, messages in shared and tensor memory); NRLDPC_NO_TM=1 selects
+    the byte-pair layout. Both must give the oracle's results."""
+    bg = nr.load_basegraph("BG1", z)
+    params = nr.code_params(bg, z, rows)
+    if stop == "crc":
+        rng = np.random.default_rng(z)
+        msgs = np.stack([nr.crc_attach(rng.integers(0, 2, params.k - 24, dtype=np.uint8), k=params.k)
+                         for _ in range(batch)])
+        tx = nr.encode_batch(msgs, bg, z, rows)[:, 2 * z:]
+        sigma = nr.ebn0_to_sigma(1.5, params.k / params.n_tx)
+        llr = nr.demap_llr(nr.bpsk_awgn(tx, sigma, rng), sigma)
+    else:
+        _, llr = noisy_llrs(bg, rows, 1.5, batch, seed=(z, rows))
+    blocks = oracle.quantize_i8(llr, z)
+    cfg = nr.DecodeConfig(max_iter=8, early_stop=stop)
+    ref = oracle.decode(blocks, bg, cfg)
+    outs, smem = [], []
+    for no_tm in (False, True):
+        if no_tm:
+            monkeypatch.setenv("NRLDPC_NO_TM", "1")
+        plan = nr.Plan(bg, rows, cfg)
+        smem.append(plan.smem_bytes)
+        out = plan.alloc_outputs(batch)
+        plan.decode_device(torch.from_numpy(blocks).cuda(), out)
+        torch.cuda.synchronize()
+        outs.append({k: v.cpu().numpy() for k, v in out.items() if v is not None})
+    assert smem[0] != smem[1]                                   # two different layouts ran
+    for o in outs:
+        assert np.array_equal(nr.unpack_bits(o["bits"], params.k), ref["bits"])
+        assert np.array_equal(o["iters"], ref["iterations"])
+        assert np.array_equal(o["synd"], ref["syndrome_weight"])
+        assert np.array_equal(o["success"].astype(bool), ref["success"])
