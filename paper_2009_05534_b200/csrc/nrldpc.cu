@@ -395,19 +395,25 @@ __device__ __forceinline__ void process_rows2(const KParams& p, uint32_t tba, ui
   b.scatter(Lg, mreg, k.one, st_ok);
 }
 
-// ---- TM layout (BG1 register-row pairs, Z in 288..384) --------------------
+// ---- TM layout (single-group pair shapes that hold an SM alone) -----------
 // L holds the biased half2 itself, 4 bytes per position ({1152+v_a,
 // 1152+v_b}; the low byte of each half is the biased byte u = v + 128), so
 // the gather needs no unpack and the scatter no pack. That doubles L
-// (104 KB at Z=384), so the messages leave shared memory: rows with w >= 7
-// keep one biased half2 per edge in shared memory (thread-major, odd word
-// stride), rows with w <= 6 in tensor memory (tcgen05.ld/st, 32x32b: the
-// thread's own TMEM lane; 3 warps share a lane quarter, each owning a
-// 170-column slot). Rows 0..5 keep their byte-pair register messages. The
-// message kind follows from the compile-time row weight (host: tm_layout).
-template <int MAXW, bool REGMSG>
+// (104 KB at BG1 Z=384), so the messages leave shared memory: rows with
+// w >= SMW keep one biased half2 per edge in shared memory (thread-major, odd
+// word stride), the other rows in tensor memory (tcgen05.ld/st, 32x32b: the
+// thread's own TMEM lane; the warps sharing a lane quarter each own a slot
+// of p.tm_slot columns). BG1 register-row shapes keep rows 0..5 in byte-pair
+// registers. The message kind follows from the compile-time row weight
+// (host: tm_shape); SMW per schedule: tm_smw.
+template <int BG, int NREG>
+__host__ __device__ constexpr int tm_smw() {
+  return BG == 2 ? 8 : NREG == 6 ? 7 : 11;
+}
+
+template <int MAXW, bool REGMSG, int SMW = 7>
 struct RowWorkTM {
-  static constexpr bool TMEM = !REGMSG && MAXW <= 6;
+  static constexpr bool TMEM = !REGMSG && MAXW < SMW;
   uint32_t off[MAXW];
   half2 t[MAXW];
   uint32_t mw[MAXW];  // the row's messages (shared / tensor memory kinds)
@@ -481,10 +487,10 @@ struct TmCtx {
   Consts k;
 };
 
-template <int W, bool REGMSG>
+template <int W, bool REGMSG, int SMW>
 __device__ __forceinline__ void process_row_tm(const KParams& p, uint32_t tb, uint32_t mb, const TmCtx& c,
                                                uint32_t* mreg, bool bar) {
-  RowWorkTM<W, REGMSG> r;
+  RowWorkTM<W, REGMSG, SMW> r;
   r.gather_pro(p, tb, mb, c.zl, c.ZL, c.Ms, c.tbase);
   if (bar) __syncthreads();
   r.gather_main(mreg, c.k.magic);
@@ -492,11 +498,11 @@ __device__ __forceinline__ void process_row_tm(const KParams& p, uint32_t tb, ui
   r.scatter(mreg, c.k.one);
 }
 
-template <int WA, int WB>
+template <int WA, int WB, int SMW>
 __device__ __forceinline__ void process_rows2_tm(const KParams& p, uint32_t tba, uint32_t mba, uint32_t tbb,
                                                  uint32_t mbb, const TmCtx& c, bool bar) {
-  RowWorkTM<WA, false> a;
-  RowWorkTM<WB, false> b;
+  RowWorkTM<WA, false, SMW> a;
+  RowWorkTM<WB, false, SMW> b;
   a.gather_pro(p, tba, mba, c.zl, c.ZL, c.Ms, c.tbase);
   b.gather_pro(p, tbb, mbb, c.zl, c.ZL, c.Ms, c.tbase);
   if (bar) __syncthreads();
@@ -773,18 +779,22 @@ __device__ __forceinline__ void one_iteration(const KParams& p, const RowCtx& c,
   }
 }
 
-// one_iteration for the TM layout (BG1, NREG == 6): same schedule, units and
-// barrier placement
-__device__ __forceinline__ void one_iteration_tm(const KParams& p, const TmCtx& c, RegMsg<6>& rm) {
+// one_iteration for the TM layout: same schedule, units and barrier placement
+template <int BG, int NREG>
+__device__ __forceinline__ void one_iteration_tm(const KParams& p, const TmCtx& c, RegMsg<NREG>& rm) {
+  constexpr int SMW = tm_smw<BG, NREG>();
+  bool bar_prev = false;
+  if constexpr (NREG == 6) {
 #pragma unroll 1
-  for (int r = 0; r < 4; r += 2) {
-    process_row_tm<19, true>(p, 5u * r, 0, c, rm.q[0], r != 0);
-    process_row_tm<19, true>(p, 5u * r + 5u, 0, c, rm.q[1], true);
-    rm.rotate2();
+    for (int r = 0; r < 4; r += 2) {
+      process_row_tm<19, true, SMW>(p, 5u * r, 0, c, rm.q[0], r != 0);
+      process_row_tm<19, true, SMW>(p, 5u * r + 5u, 0, c, rm.q[1], true);
+      rm.rotate2();
+    }
+    process_row_tm<3, true, SMW>(p, 20u, 0, c, rm.r4, true);
+    process_row_tm<8, true, SMW>(p, 21u, 0, c, rm.r5, true);
+    bar_prev = true;
   }
-  process_row_tm<3, true>(p, 20u, 0, c, rm.r4, true);
-  process_row_tm<8, true>(p, 21u, 0, c, rm.r5, true);
-  bool bar_prev = true;
   uint32_t ncode = p.unit_a[0].x;
 #pragma unroll 1
   for (int u = 0; u < p.n_units; ++u) {
@@ -792,10 +802,10 @@ __device__ __forceinline__ void one_iteration_tm(const KParams& p, const TmCtx& 
     const uint4 A = p.unit_a[u];
     const uint4 B = p.unit_b[u];
     ncode = p.unit_a[u + 1].x;
-    dispatch_unit<1, 6>(code, [&](auto WA, auto WB) {
+    dispatch_unit<BG, NREG>(code, [&](auto WA, auto WB) {
       constexpr int wa = decltype(WA)::value, wb = decltype(WB)::value;
-      if constexpr (wb == 0) process_row_tm<wa, false>(p, A.z, A.w, c, nullptr, bar_prev);
-      else process_rows2_tm<wa, wb>(p, A.z, A.w, B.x, B.y, c, bar_prev);
+      if constexpr (wb == 0) process_row_tm<wa, false, SMW>(p, A.z, A.w, c, nullptr, bar_prev);
+      else process_rows2_tm<wa, wb, SMW>(p, A.z, A.w, B.x, B.y, c, bar_prev);
     });
     bar_prev = A.y != 0;
   }
@@ -805,6 +815,7 @@ __device__ __forceinline__ void one_iteration_tm(const KParams& p, const TmCtx& 
 }
 
 // local_check for the TM layout (Z % 32 == 0, one group)
+template <int BG>
 __device__ __forceinline__ void local_check_tm(const KParams& p, uint32_t zl, uint32_t ZL, uint32_t Ls, int* wcnt,
                                                int* mabs, bool early, bool need_a, bool need_b) {
   int wa = 0, wb = 0;
@@ -814,7 +825,7 @@ __device__ __forceinline__ void local_check_tm(const KParams& p, uint32_t zl, ui
     const int e0 = p.row_start[r];
     const int t0 = p.tab_start[r];
     const int w = p.row_start[r + 1] - e0;
-    dispatch_w<1>(w, [&](auto W) { row_parity_tm<decltype(W)::value>(p, t0 / 4u, zl, ZL, wa, wb); });
+    dispatch_w<BG>(w, [&](auto W) { row_parity_tm<decltype(W)::value>(p, t0 / 4u, zl, ZL, wa, wb); });
     if (early) {
       const bool fa = !need_a || __any_sync(0xFFFFFFFFu, wa != 0);
       const bool fb = !need_b || __any_sync(0xFFFFFFFFu, wb != 0);
@@ -954,7 +965,7 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
                                                                    const int8_t* __restrict__ llr, KOut o) {
   static_assert(NREG == 0 || (BG == 1 && LANES == 2), "register messages: BG1 pairs only");
   static_assert(!ABS || BG != 0, "absolute addressing: compile-time schedules only");
-  static_assert(!TM || (BG == 1 && LANES == 2 && NREG == 6 && ABS), "TM layout: BG1 register-row pairs");
+  static_assert(!TM || (BG != 0 && LANES == 2 && (NREG == 6 || NREG == 0) && ABS), "TM layout: pair shapes");
   constexpr uint32_t ES = TM ? 4 : LANES;  // bytes per position of L
   extern __shared__ __align__(16) uint8_t smem[];
   uint16_t* lut = reinterpret_cast<uint16_t*>(smem);
@@ -1015,8 +1026,8 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const int warp = tid >> 5;
-    // 3 warps per lane quarter, 170 columns each (host: tm_layout)
-    tbase = lds_u32(&cta->kc[5]) + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * 170u;
+    // the warps of a lane quarter own consecutive slots (host: tm_shape)
+    tbase = lds_u32(&cta->kc[5]) + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * p.tm_slot;
   }
 
   bool lane_valid[2];
@@ -1129,7 +1140,7 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
   RegMsg<NREG> rm;
   rm.init();
   for (int it = 1; it <= p.max_iter; ++it) {
-    if constexpr (TM) one_iteration_tm(p, tc, rm);
+    if constexpr (TM) one_iteration_tm<BG, NREG>(p, tc, rm);
     else one_iteration<BG, MAXW, LANES, NREG, ABS>(p, rc, rm);
     const bool last = it == p.max_iter;
     if (!(p.early_stop != NRLDPC_STOP_NONE || p.trace || last)) continue;
@@ -1140,7 +1151,7 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
       // weights are only needed in full when traced or final
       const bool early = BG != 0 && !p.trace && !last && p.z % 32 == 0;
       if constexpr (TM)
-        local_check_tm(p, zl, ZL, p.abs_base, wc, ma, early, lane_valid[0] && !gs.done[0],
+        local_check_tm<BG>(p, zl, ZL, p.abs_base, wc, ma, early, lane_valid[0] && !gs.done[0],
                        lane_valid[1] && !gs.done[1]);
       else
         local_check<BG, MAXW, LANES, ABS>(p, zl, ZL, Lg, wc, ma, early, lane_valid[0] && !gs.done[0],
@@ -1263,7 +1274,7 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const 
                                                                           const int8_t* __restrict__ llr, KOut o) {
   constexpr int LANES = 2;
   constexpr bool ABS = true;
-  static_assert(!TM || (BG == 1 && NREG == 6), "TM layout: BG1 register-row pairs");
+  static_assert(!TM || NREG == 6 || NREG == 0, "TM layout: pair shapes");
   constexpr uint32_t ES = TM ? 4 : LANES;  // bytes per position of L
   extern __shared__ __align__(16) uint8_t smem[];
   LaneState* ls = reinterpret_cast<LaneState*>(smem);  // the (unused) beta-table area
@@ -1307,7 +1318,7 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const 
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const int warp = tid >> 5;
-    tbase = lds_u32(&cta->kc[5]) + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * 170u;
+    tbase = lds_u32(&cta->kc[5]) + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * p.tm_slot;
   }
   // messages: all zero (biased)
   {
@@ -1411,7 +1422,7 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const 
   rm.init();
   int it[2] = {0, 0};
   while (cw[0] >= 0 || cw[1] >= 0) {
-    if constexpr (TM) one_iteration_tm(p, tc, rm);
+    if constexpr (TM) one_iteration_tm<BG, NREG>(p, tc, rm);
     else one_iteration<BG, MAXW, LANES, NREG, ABS>(p, rc, rm);
     bool act[2], last[2];
 #pragma unroll
@@ -1422,7 +1433,7 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const 
     }
     {
       int wc[2], ma[2];
-      if constexpr (TM) local_check_tm(p, zl, ZL, p.abs_base, wc, ma, !last[0] && !last[1], act[0], act[1]);
+      if constexpr (TM) local_check_tm<BG>(p, zl, ZL, p.abs_base, wc, ma, !last[0] && !last[1], act[0], act[1]);
       else local_check<BG, MAXW, LANES, ABS>(p, zl, ZL, Lg, wc, ma, !last[0] && !last[1], act[0], act[1]);
 #pragma unroll
       for (int l = 0; l < 2; ++l) {
@@ -2066,22 +2077,32 @@ Shape choose_shape(const nrldpc_plan* p, int max_lanes) {
   return sh;
 }
 
-// TM layout of a register-row shape (k_decode_i8 TM): L as biased half2,
-// messages of rows >= 6 with w >= 7 in shared memory (one half2 per edge,
-// odd word stride) and w <= 6 in tensor memory (one column per edge, at most
-// 170 columns per thread). Returns the byte-pair shape unchanged when the
-// layout does not fit; NRLDPC_NO_TM=1 disables it.
-constexpr uint32_t kTmColsPerThread = 170;
+// TM layout (k_decode_i8 TM) of a single-group pair shape that holds an SM
+// alone: L as biased half2, messages of rows >= nreg with w >= SMW in
+// shared memory (one half2 per edge, odd word stride) and the others in
+// tensor memory (one column per edge). The CTA allocates all 512 TMEM
+// columns, so the shape keeps one CTA per SM (shared memory is padded to
+// force it). Returns the byte-pair shape unchanged when the layout does not
+// apply or fit; NRLDPC_NO_TM=1 disables it.
 Shape tm_shape(const nrldpc_plan* p, const Shape& leg) {
-  if (leg.nreg != 6 || !leg.abs || leg.groups != 1 || p->z % 32 != 0 || p->z > 384 || getenv("NRLDPC_NO_TM"))
+  const size_t smem_max = 232448, one_per_sm = smem_max / 2 + 1024;
+  if (!leg.abs || leg.groups != 1 || leg.lanes != 2 || p->z % 32 != 0 || p->z > 384 || getenv("NRLDPC_NO_TM"))
     return leg;
-  const size_t smem_max = 232448;
+  int smw = 0;
+  if (p->schedule == 1 && leg.nreg == 6) smw = tm_smw<1, 6>();
+  else if (p->schedule == 1 && leg.nreg == 0) smw = tm_smw<1, 0>();
+  else if (p->schedule == 2 && leg.nreg == 0) smw = tm_smw<2, 0>();
+  // byte-pair shapes with several CTAs per SM keep them (register-row shapes
+  // hold an SM alone through their register count)
+  if (!smw || (leg.nreg == 0 && leg.smem < one_per_sm)) return leg;
+  const int warps = p->z / 32;
+  const uint32_t slot = 512u / (uint32_t)((warps + 3) / 4);
   const KParams& b = p->base;
   MsgLayout ml{};
   uint32_t sm_slots = 0, tm_cols = 0;
-  for (int r = 6; r < p->rows; ++r) {
+  for (int r = leg.nreg; r < p->rows; ++r) {
     const int w = b.row_start[r + 1] - b.row_start[r];
-    if (w >= 7) {
+    if (w >= smw) {
       ml.mb[r] = sm_slots * 4u;
       sm_slots += (uint32_t)w;
     } else {
@@ -2089,7 +2110,7 @@ Shape tm_shape(const nrldpc_plan* p, const Shape& leg) {
       tm_cols += (uint32_t)w;
     }
   }
-  if (tm_cols > kTmColsPerThread) return leg;
+  if (tm_cols > slot) return leg;
   uint32_t e = sm_slots | 1u;  // odd word stride: conflict-free across z
   const size_t lb = align16((size_t)p->n_blocks * p->z * 4);
   const size_t mb = align16((size_t)p->z * e * 4);
@@ -2097,12 +2118,13 @@ Shape tm_shape(const nrldpc_plan* p, const Shape& leg) {
   Shape sh = leg;
   sh.tm = true;
   sh.occ = 0;
-  sh.smem = smem_for(1, lb, mb);
+  sh.smem = std::max(smem_for(1, lb, mb), one_per_sm);
   sh.kp.l_bytes = (uint32_t)lb;
   sh.kp.m_bytes = (uint32_t)mb;
   sh.kp.m_stride = e * 4u;
   sh.kp.tm_cols = tm_cols;
-  build_units(p, 6, ml, sh.kp);
+  sh.kp.tm_slot = slot;
+  build_units(p, leg.nreg, ml, sh.kp);
   for (int t = 0; t < NR_MAX_TAB; ++t) {
     sh.kp.sh[t] = b.sh[t] * 4u;
     sh.kp.cb[t] = b.cb[t] * (uint32_t)p->z * 4u + sh.kp.abs_base;
@@ -2162,7 +2184,9 @@ static cudaError_t launch_shape(const nrldpc_plan* plan, Shape& sh, const int8_t
                       sh.groups == 1 && plan->z % 32 == 0 && !getenv("NRLDPC_NO_REFILL");
   if (refill && (in == nullptr || batch > 2)) {
     cudaError_t e = cudaSuccess;
-    if (sh.tm) e = launch_refill<1, 19, 6, true>(sh, dev, in, batch, o, st);
+    if (sh.tm && sh.nreg == 6) e = launch_refill<1, 19, 6, true>(sh, dev, in, batch, o, st);
+    else if (sh.tm && plan->schedule == 1) e = launch_refill<1, 19, 0, true>(sh, dev, in, batch, o, st);
+    else if (sh.tm) e = launch_refill<2, 10, 0, true>(sh, dev, in, batch, o, st);
     else if (plan->schedule == 1 && sh.nreg == 6) e = launch_refill<1, 19, 6>(sh, dev, in, batch, o, st);
     else if (plan->schedule == 1 && sh.nreg == 0) e = launch_refill<1, 19, 0>(sh, dev, in, batch, o, st);
     else if (plan->schedule == 2 && sh.nreg == 0) e = launch_refill<2, 10, 0>(sh, dev, in, batch, o, st);
@@ -2170,7 +2194,11 @@ static cudaError_t launch_shape(const nrldpc_plan* plan, Shape& sh, const int8_t
     if (in != nullptr || e != cudaSuccess) return e;
   }
 plain:
-  if (sh.tm) return launch_i8<1, 19, 2, 6, true, true>(sh, dev, in, batch, o, st);
+  if (sh.tm) {
+    if (sh.nreg == 6) return launch_i8<1, 19, 2, 6, true, true>(sh, dev, in, batch, o, st);
+    if (plan->schedule == 1) return launch_i8<1, 19, 2, 0, true, true>(sh, dev, in, batch, o, st);
+    return launch_i8<2, 10, 2, 0, true, true>(sh, dev, in, batch, o, st);
+  }
   switch (plan->schedule) {
     case 1:
       if (!two) return launch_i8<1, 19, 1>(sh, dev, in, batch, o, st);

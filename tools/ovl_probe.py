@@ -1,0 +1,16 @@
+import os, sys, json
+sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tools")
+import numpy as np, torch
+import paper_2009_05534_b200 as nr
+from bench_configs import gpu_blocks, overlapped_ms, time_plan
+res = {}
+for bgn, z in ((2, 384), (1, 256), (1, 384)):
+    bg = nr.load_basegraph(bgn, z)
+    plan = nr.Plan(bg, bg.m_bg, nr.DecodeConfig(max_iter=10, early_stop="none"))
+    _, blocks = gpu_blocks(bg, bg.m_bg, 2.0, 1024, 1)
+    out = plan.alloc_outputs(1024)
+    r = {"smem": plan.smem_bytes, "single": round(float(np.median(time_plan(plan, blocks, out, 30))), 4)}
+    for ns in (1, 2, 3):
+        r[f"ovl{ns}"] = [round(float(overlapped_ms(plan, blocks, 1024, nstreams=ns)), 4) for _ in range(2)]
+    res[f"bg{bgn}_z{z}"] = r
+print(os.environ.get("NRLDPC_NO_TM", "tm"), json.dumps(res))
