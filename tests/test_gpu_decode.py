@@ -535,14 +535,18 @@ def test_scratch_paths_capture_and_concurrent_streams(cuda_ok, prec, stop):
     check(out)
 
 
-@pytest.mark.parametrize("z,rows,stop,batch", [(384, 46, "none", 64), (288, 46, "none", 37), (320, 9, "none", 20),
-                                                (352, 46, "syndrome", 2), (384, 30, "crc", 2),
-                                                (384, 6, "none", 8), (384, 7, "none", 8)])
-def test_tm_layout_matches_byte_pair_layout_and_oracle(cuda_ok, z, rows, stop, batch, monkeypatch):
-    """BG1 register-row pairs (Z = 288..384) decode on the TM layout (half2
-    posteriors, messages in shared and tensor memory); NRLDPC_NO_TM=1 selects
-    the byte-pair layout. Both must give the oracle's results."""
-    bg = nr.load_basegraph("BG1", z)
+@pytest.mark.parametrize("bg_id,z,rows,stop,batch", [
+    ("BG1", 384, 46, "none", 64), ("BG1", 288, 46, "none", 37), ("BG1", 320, 9, "none", 20),
+    ("BG1", 352, 46, "syndrome", 2), ("BG1", 384, 30, "crc", 2), ("BG1", 384, 6, "none", 8),
+    ("BG1", 384, 7, "none", 8), ("BG1", 256, 46, "none", 33), ("BG1", 160, 46, "syndrome", 64),
+    ("BG1", 224, 46, "none", 9), ("BG2", 384, 42, "none", 40), ("BG2", 256, 42, "syndrome", 65),
+    ("BG2", 320, 42, "crc", 2)])
+def test_tm_layout_matches_byte_pair_layout_and_oracle(cuda_ok, bg_id, z, rows, stop, batch, monkeypatch):
+    """Single-group pair shapes that hold an SM alone decode on the TM layout
+    (half2 posteriors, messages in shared and tensor memory; the lane-refill
+    kernel too for early stops with batch > 2); NRLDPC_NO_TM=1 selects the
+    byte-pair layout. Both must give the oracle's results."""
+    bg = nr.load_basegraph(bg_id, z)
     params = nr.code_params(bg, z, rows)
     if stop == "crc":
         rng = np.random.default_rng(z)
