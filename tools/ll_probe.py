@@ -24,7 +24,8 @@ from bench_configs import spot_check, time_plan  # noqa: E402
 from paper_2009_05534_b200.synth import noisy_llrs  # noqa: E402
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 200
-cases = [("BG1", 384, 46, "BG1 R=1/3"), ("BG2", 384, 42, "BG2 R=1/5"), ("BG2", 64, 42, "BG2 Z=64 R=1/5")]
+cases = [("BG1", 384, 46, "BG1 R=1/3"), ("BG2", 384, 42, "BG2 R=1/5"), ("BG2", 64, 42, "BG2 Z=64 R=1/5"),
+         ("BG1", 128, 46, "BG1 Z=128"), ("BG2", 192, 42, "BG2 Z=192"), ("BG1", 16, 46, "BG1 Z=16")]
 out_lines = []
 for name, z, rows, label in cases:
     bg = nr.load_basegraph(name, z)
