@@ -105,3 +105,78 @@ def decode_mixed_sharded(groups, llrs: list, cfg, decode_fn=None, group=None):
     for part in gathered:
         merged.update(part)
     return [merged[i] for i in range(len(groups))]
+
+
+class MultiDeviceDecoder:
+    """One process driving several GPUs (north_star subsystem 5):
+    a host batch splits into contiguous shards, one per device, and every
+    device decodes its shard through its own plan -- its own streams, staging
+    slots and pinned result buffers -- concurrently with the others. No
+    process group and no NCCL: the shards never communicate, and the results
+    merge in shard order, so the output equals one ``decode`` of the whole
+    batch.
+
+    ``devices``: CUDA device indices (default: all visible). A device may
+    appear more than once (several plans on one GPU). Inputs are int8 host
+    blocks (B, n_c); pass pinned arrays (``pinned_input``) for the copies to
+    overlap fully. ``plan_factory(device)`` lets tests substitute the plan."""
+
+    def __init__(self, bg, rows_used: int, cfg, devices=None, chunks: int = 12, plan_factory=None):
+        from concurrent.futures import ThreadPoolExecutor
+
+        from .decoder import Plan, _coerce_cfg
+
+        self.cfg = _coerce_cfg(cfg)
+        if devices is None:
+            import torch
+            devices = list(range(torch.cuda.device_count()))
+        if not devices:
+            raise ValueError("need at least one device")
+        self.devices = [int(d) for d in devices]
+        factory = plan_factory or (lambda d: Plan(bg, rows_used, self.cfg, device=d))
+        self.plans = [factory(d) for d in self.devices]
+        self.k = self.plans[0].k
+        self.chunks = int(chunks)
+        self._pool = ThreadPoolExecutor(max_workers=len(self.plans))
+        self._out = [None] * len(self.plans)
+
+    def close(self) -> None:
+        self._pool.shutdown(wait=True)
+
+    def pinned_input(self, batch: int, n_c: int) -> np.ndarray:
+        """A pinned int8 host array (batch, n_c) to fill and pass to decode."""
+        import torch
+        return torch.empty((batch, n_c), dtype=torch.int8, pin_memory=True).numpy()
+
+    def _run(self, i: int, part: np.ndarray) -> dict:
+        plan = self.plans[i]
+        b = part.shape[0]
+        out = self._out[i]
+        if out is None or out["iters"].shape[0] < b:
+            out = self._out[i] = plan.host_outputs(max(b, 1), pinned=True)
+        if b == 0:
+            return {k: v[:0] for k, v in out.items()}
+        view = {k: v[:b] for k, v in out.items()}
+        plan.decode_host(part, chunks=max(1, min(self.chunks, b // 86)), out=view)
+        return {k: v.copy() for k, v in view.items()}
+
+    def decode(self, llrs) -> DecodeResult:
+        """Decode (B, n_c) int8 blocks; same result as ``decode(llrs, bg, cfg)``."""
+        from .decoder import EarlyStop, _empty_result, unpack_bits
+
+        arr = np.asarray(llrs)
+        if arr.ndim == 1:
+            arr = arr[None, :]
+        if arr.dtype != np.int8:
+            raise ValueError("MultiDeviceDecoder takes int8 blocks")
+        arr = np.ascontiguousarray(arr)
+        n = len(self.plans)
+        bounds = [shard_bounds(arr.shape[0], n, i) for i in range(n)]
+        futs = [self._pool.submit(self._run, i, arr[lo:hi]) for i, (lo, hi) in enumerate(bounds)]
+        outs = [f.result() for f in futs]  # re-raises a shard's error
+        crc = self.cfg.early_stop is EarlyStop.CRC
+        parts = [DecodeResult(bits=unpack_bits(o["bits"], self.k), iterations=o["iters"].astype(np.int64),
+                              success=o["success"].astype(bool), syndrome_weight=o["synd"].astype(np.int64),
+                              crc_ok=o["crc_ok"].astype(bool) if crc else None)
+                 for o in outs if o["iters"].shape[0]]
+        return merge_results(parts) if parts else _empty_result(self.k, self.cfg)

@@ -576,3 +576,39 @@ def test_tm_layout_matches_byte_pair_layout_and_oracle(cuda_ok, bg_id, z, rows, 
         assert np.array_equal(o["iters"], ref["iterations"])
         assert np.array_equal(o["synd"], ref["syndrome_weight"])
         assert np.array_equal(o["success"].astype(bool), ref["success"])
+
+
+@pytest.mark.parametrize("bg_id,z,stop,batch,devices", [("BG1", 384, "none", 301, [0, 0]),
+                                                        ("BG2", 384, "syndrome", 257, [0, 0, 0]),
+                                                        ("BG2", 52, "crc", 2, [0, 0, 0])])
+def test_multi_device_decoder_matches_single_decode(cuda_ok, bg_id, z, stop, batch, devices):
+    """One process, several plans (per-device streams and pinned buffers, no
+    process group): shards merge to exactly the single-call result. One GPU
+    here, so the plans share device 0."""
+    from paper_2009_05534_b200.shard import MultiDeviceDecoder
+
+    bg = nr.load_basegraph(bg_id, z)
+    params = nr.code_params(bg, z, bg.m_bg)
+    if stop == "crc":
+        rng = np.random.default_rng(z)
+        msgs = np.stack([nr.crc_attach(rng.integers(0, 2, params.k - 24, dtype=np.uint8), k=params.k)
+                         for _ in range(batch)])
+        tx = nr.encode_batch(msgs, bg, z, bg.m_bg)[:, 2 * z:]
+        sigma = nr.ebn0_to_sigma(2.0, params.k / params.n_tx)
+        llr = nr.demap_llr(nr.bpsk_awgn(tx, sigma, rng), sigma)
+    else:
+        _, llr = noisy_llrs(bg, bg.m_bg, 1.0, batch, seed=(z, 11))
+    blocks = oracle.quantize_i8(llr, z)
+    cfg = nr.DecodeConfig(max_iter=10, early_stop=stop)
+    dec = MultiDeviceDecoder(bg, bg.m_bg, cfg, devices=devices)
+    try:
+        pinned = dec.pinned_input(batch, params.n_c)
+        pinned[:] = blocks
+        res = dec.decode(pinned)
+    finally:
+        dec.close()
+    ref = nr.decode(blocks, bg, cfg)
+    assert np.array_equal(res.bits, ref.bits) and np.array_equal(res.iterations, ref.iterations)
+    assert np.array_equal(res.syndrome_weight, ref.syndrome_weight) and np.array_equal(res.success, ref.success)
+    if stop == "crc":
+        assert np.array_equal(res.crc_ok, ref.crc_ok)

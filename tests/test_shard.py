@@ -110,3 +110,46 @@ def test_gloo_mixed_groups_match_single_process(tmp_path):
     for i, (b, z, rows) in enumerate(shapes):
         ref = oracle.decode(blocks[i], nr.load_basegraph(b, z), nr.DecodeConfig(max_iter=6), threads=1)
         assert np.array_equal(got[f"b{i}"], ref["bits"]) and np.array_equal(got[f"i{i}"], ref["iterations"])
+
+
+class _OraclePlan:
+    """Stands in for a device plan: decode_host fills the result buffers from the CPU oracle."""
+
+    def __init__(self, bg, cfg):
+        self.bg, self.cfg = bg, cfg
+        self.k = bg.k_b * bg.z
+        self.words = (self.k + 31) // 32
+
+    def host_outputs(self, batch, pinned=False):
+        return {"bits": np.zeros((batch, self.words), np.uint32), "iters": np.zeros(batch, np.int32),
+                "synd": np.zeros(batch, np.int32), "success": np.zeros(batch, np.uint8),
+                "crc_ok": np.zeros(batch, np.uint8)}
+
+    def decode_host(self, llr, chunks=4, out=None):
+        ref = oracle.decode(llr, self.bg, self.cfg)
+        packed = np.packbits(ref["bits"], axis=1, bitorder="little")
+        packed = np.pad(packed, ((0, 0), (0, 4 * self.words - packed.shape[1])))
+        out["bits"][:] = packed.view("<u4")
+        out["iters"][:] = ref["iterations"]
+        out["synd"][:] = ref["syndrome_weight"]
+        out["success"][:] = ref["success"]
+        return out
+
+
+@pytest.mark.parametrize("batch,devices", [(7, [0, 1, 2]), (2, [0, 1, 2]), (5, [3])])
+def test_multi_device_decoder_shards_and_merges_in_order(batch, devices):
+    from paper_2009_05534_b200.shard import MultiDeviceDecoder
+
+    bg = nr.load_basegraph("BG2", 16)
+    cfg = nr.DecodeConfig(max_iter=6, early_stop="syndrome")
+    _, llr = noisy_llrs(bg, bg.m_bg, 1.0, batch, seed=(batch, 9))
+    blocks = oracle.quantize_i8(llr, 16)
+    dec = MultiDeviceDecoder(bg, bg.m_bg, cfg, devices=devices, plan_factory=lambda d: _OraclePlan(bg, cfg))
+    try:
+        res = dec.decode(blocks)
+    finally:
+        dec.close()
+    ref = oracle.decode(blocks, bg, cfg)
+    assert np.array_equal(res.bits, ref["bits"])
+    assert np.array_equal(res.iterations, ref["iterations"])
+    assert np.array_equal(res.syndrome_weight, ref["syndrome_weight"])
