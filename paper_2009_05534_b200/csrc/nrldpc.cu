@@ -419,7 +419,7 @@ struct RowWorkTM {
   uint32_t mw[MAXW];  // the row's messages (shared / tensor memory kinds)
   half2 m1, m2;
   uint32_t S;
-  uint32_t Ma;  // shared address (w >= 7) or tensor-memory address (w <= 6) of the row's messages
+  uint32_t Ma;  // shared address (w >= SMW) or tensor-memory address (w < SMW) of the row's messages
 
   // thread-private part (tables, addresses, own messages): may run before the
   // barrier that closes the previous layer
