@@ -1952,6 +1952,55 @@ MsgLayout msg_layout(const nrldpc_plan* p, int nreg, int e_reg, int lanes, bool 
   return m;
 }
 
+// On-chip message variant of a float shape (k_decode_flt FTM): single-group
+// BG1/BG2 shapes (Z % 32 == 0, Z <= 384). Rows by ftm_kind: global rows keep
+// workspace slots (they must be the leading rows: e_reg edges), shared rows
+// one word per edge in a thread-major row (odd word stride), tensor rows one
+// TMEM column per edge. Expects build_units to run with the returned layout;
+// returns false (shape unchanged) when the layout does not fit.
+// NRLDPC_NO_TM=1 disables it.
+bool ftm_layout(const nrldpc_plan* p, Shape& sh, MsgLayout& ml) {
+  if (p->schedule == 0 || sh.groups != 1 || p->z % 32 != 0 || p->z > 384 || getenv("NRLDPC_NO_TM")) return false;
+  const size_t smem_max = 232448, one_per_sm = smem_max / 2 + 1024;
+  const KParams& b = p->base;
+  const int warps = p->z / 32;
+  const uint32_t slot = 512u / (uint32_t)((warps + 3) / 4);
+  uint32_t sm_slots = 0, tm_cols = 0;
+  int e_glob = 0;
+  bool leading = true;
+  for (int r = 0; r < p->rows; ++r) {
+    const int w = b.row_start[r + 1] - b.row_start[r];
+    const int kind = p->schedule == 1 ? ftm_kind<1>(w) : ftm_kind<2>(w);
+    if (kind == 0) {
+      if (!leading) return false;
+      ml.mb[r] = (uint32_t)b.row_start[r];
+      e_glob = b.row_start[r + 1];
+    } else {
+      leading = false;
+      if (kind == 1) {
+        ml.mb[r] = sm_slots * 4u;
+        sm_slots += (uint32_t)w;
+      } else {
+        ml.mb[r] = tm_cols;
+        tm_cols += (uint32_t)w;
+      }
+    }
+  }
+  if (tm_cols > slot) return false;
+  const uint32_t e = sm_slots | 1u;
+  const size_t mb = align16((size_t)p->z * e * 4);
+  const size_t need = sh.smem + mb;  // header + L (one group) + shared message rows
+  if (need > smem_max) return false;
+  sh.tm = true;
+  sh.smem = std::max(need, one_per_sm);
+  sh.kp.m_bytes = (uint32_t)mb;
+  sh.kp.m_stride = e * 4u;
+  sh.kp.e_reg = e_glob;
+  sh.kp.tm_cols = tm_cols;
+  sh.kp.tm_slot = slot;
+  return true;
+}
+
 void build_units(const nrldpc_plan* p, int nreg, const MsgLayout& ml, KParams& kp) {
   const KParams& b = p->base;
   int n = 0;
@@ -2220,11 +2269,11 @@ plain:
   }
 }
 
-template <int PREC, int BG>
+template <int PREC, int BG, bool FTM = false>
 static cudaError_t launch_float_bg(Shape& sh, int device, const void* llr, long long batch, const KOut& o,
                                 cudaStream_t st) {
   static bool attr_done[64] = {};
-  auto kern = k_decode_flt<PREC, BG>;
+  auto kern = k_decode_flt<PREC, BG, FTM>;
   if (!attr_done[device & 63]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (e != cudaSuccess) return e;
@@ -2242,9 +2291,10 @@ static cudaError_t launch_float_bg(Shape& sh, int device, const void* llr, long 
   kp.trace = o.trace_w != nullptr;
   const long long per_cta = (long long)sh.groups * sh.lanes;
   const long long grid = (batch + per_cta - 1) / per_cta;
-  // messages: stream-ordered workspace, [group][edge][z] x 4 bytes
+  // messages: stream-ordered workspace, [group][edge][z] x 4 bytes (FTM:
+  // only the rows kept in global memory)
   uint32_t* ws = nullptr;
-  const size_t ws_bytes = (size_t)grid * sh.groups * kp.n_edges * kp.z * 4;
+  const size_t ws_bytes = std::max<size_t>(16, (size_t)grid * sh.groups * (FTM ? kp.e_reg : kp.n_edges) * kp.z * 4);
   cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&ws), ws_bytes, device, st);
   if (e != cudaSuccess) return e;
   kern<<<(unsigned)grid, sh.threads, sh.smem, st>>>(kp, llr, ws, o);
@@ -2258,8 +2308,10 @@ static cudaError_t launch_float_bg(Shape& sh, int device, const void* llr, long 
 template <int PREC>
 static cudaError_t launch_float(int schedule, Shape& sh, int device, const void* llr, long long batch,
                                 const KOut& o, cudaStream_t st) {
-  if (schedule == 1) return launch_float_bg<PREC, 1>(sh, device, llr, batch, o, st);
-  if (schedule == 2) return launch_float_bg<PREC, 2>(sh, device, llr, batch, o, st);
+  if (schedule == 1) return sh.tm ? launch_float_bg<PREC, 1, true>(sh, device, llr, batch, o, st)
+                                  : launch_float_bg<PREC, 1>(sh, device, llr, batch, o, st);
+  if (schedule == 2) return sh.tm ? launch_float_bg<PREC, 2, true>(sh, device, llr, batch, o, st)
+                                  : launch_float_bg<PREC, 2>(sh, device, llr, batch, o, st);
   return launch_float_bg<PREC, 0>(sh, device, llr, batch, o, st);
 }
 
@@ -2623,9 +2675,11 @@ int nrldpc_plan_create(int device, int k_b, int z, int rows_used, const int32_t*
   } else {
     p->main = choose_shape_float(p);
     if (p->schedule != 0) {
-      // layer units with messages addressed by edge index ([edge][z] workspace)
+      // layer units with messages addressed by edge index ([edge][z]
+      // workspace), or by their on-chip slots
       MsgLayout ml{};
-      for (int r = 0; r < p->rows; ++r) ml.mb[r] = (uint32_t)p->base.row_start[r];
+      if (!ftm_layout(p, p->main, ml))
+        for (int r = 0; r < p->rows; ++r) ml.mb[r] = (uint32_t)p->base.row_start[r];
       build_units(p, 0, ml, p->main.kp);
     }
     if (precision == NRLDPC_F32) {

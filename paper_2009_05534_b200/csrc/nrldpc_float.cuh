@@ -7,7 +7,11 @@
 // codewords per half2 lane; f32 one codeword per thread. Posteriors live in
 // shared memory (4 bytes per position per group); messages (4 bytes per edge
 // and z per group) live in a stream-ordered global workspace, coalesced as
-// [group][edge][z]. Included by nrldpc.cu.
+// [group][edge][z]. On-chip variant (FTM, single-group BG1/BG2 shapes that
+// hold an SM alone): the messages of most rows move on chip, into shared
+// memory (thread-major, odd word stride) or tensor memory (tcgen05.ld/st,
+// the thread's own lane, as in k_decode_i8's TM layout); the kind follows
+// from the row weight (ftm_kind). Included by nrldpc.cu.
 #pragma once
 
 namespace nr {
@@ -69,29 +73,50 @@ struct FOps<NRLDPC_F16> {
   }
 };
 
+// Message store of a row in the on-chip variant: 0 global workspace, 1 shared
+// memory, 2 tensor memory. BG1: the four 19-edge core rows (76 edges) stay
+// global, rows with w >= 7 go to shared memory, the rest to tensor memory;
+// BG2: w >= 8 shared, the rest tensor memory (host: ftm_shape).
+template <int BG>
+__host__ __device__ constexpr int ftm_kind(int w) {
+  return BG == 1 ? (w == 19 ? 0 : w >= 7 ? 1 : 2) : (w >= 8 ? 1 : 2);
+}
+
 // One row of a compile-time (BG1/BG2) layer unit in the float engines,
 // split like the int8 RowWork: pro() touches only this thread's own state
 // (graph tables, edge addresses, its messages from the global workspace), so
 // it runs before the barrier that closes the previous layer; main() reads
 // the posteriors.
-template <int PREC, int W>
+template <int PREC, int W, int KIND = 0>
 struct FRow {
   using F = FOps<PREC>;
   uint32_t off[W], t[W], neg[W], msg[W];
   uint32_t m1, m2, S, b1, b2;
-  uint32_t* Me;  // this row's first edge: edge j at Me[j * Z]
+  uint32_t* Me;  // global kind: this row's first edge, edge j at Me[j * Z]
+  uint32_t Ma;   // shared kind: shared address of the row's first message; tensor kind: TMEM address
+  // e0: the row's first edge (global kind), byte offset in this thread's
+  // shared message row (shared kind) or column in its TMEM slot (tensor kind)
   __device__ __forceinline__ void pro(const KParams& p, uint32_t tq, uint32_t e0, uint32_t zl, uint32_t ZL,
-                                      uint32_t* Mg, bool active) {
+                                      uint32_t* Mg, bool active, uint32_t Ms = 0, uint32_t tbase = 0) {
     uint32_t tsh[W], tcb[W];
     load_row_tables<W>(p, tq, W, tsh, tcb);
-    Me = Mg + (long long)e0 * p.z;
+    if constexpr (KIND == 0) {
+      Me = Mg + (long long)e0 * p.z;
+    } else if constexpr (KIND == 1) {
+      Ma = Ms + e0;
+    } else {
+      Ma = tbase + e0;
+      tm_ld_row<W>(Ma, msg);
+    }
 #pragma unroll
     for (int j = 0; j < W; ++j) {
       off[j] = edge_offset(tsh[j], tcb[j], zl, ZL);
-      msg[j] = active ? Me[(long long)j * p.z] : 0u;
+      if constexpr (KIND == 0) msg[j] = active ? Me[(long long)j * p.z] : 0u;
+      if constexpr (KIND == 1) msg[j] = lds_u32(Ma + 4u * j);
     }
   }
   __device__ __forceinline__ void main(const uint8_t* Lg, uint32_t beta) {
+    if constexpr (KIND == 2) tm_wait_ld<W>(msg);
     m1 = F::sat();
     m2 = F::sat();
     S = 0;
@@ -114,11 +139,14 @@ struct FRow {
       const uint32_t eq = F::eq_mask(F::absv(t[j]), m1);        // the argmin edge (ties: m1 == m2)
       const uint32_t mag = (eq & b2) | (~eq & b1);
       const uint32_t out = mag ^ ((S ^ neg[j]) & F::sign);       // -mag flips the sign bit
+      if constexpr (KIND == 2) msg[j] = out;
       if (active) {
-        Me[(long long)j * p.z] = out;
+        if constexpr (KIND == 0) Me[(long long)j * p.z] = out;
+        if constexpr (KIND == 1) sts_u32(Ma + 4u * j, out);
         *reinterpret_cast<uint32_t*>(Lg + off[j]) = F::add_clamp(t[j], out);  // decoder.py:318
       }
     }
+    if constexpr (KIND == 2) tm_st_row<W>(Ma, msg);  // warp-collective: every thread of an FTM CTA is active
   }
 };
 
@@ -129,10 +157,11 @@ struct FltState {
   uint32_t accept[2];
 };
 
-template <int PREC, int BG = 0>
+template <int PREC, int BG = 0, bool FTM = false>
 __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KParams p,
                                                     const void* __restrict__ llr,
                                                     uint32_t* __restrict__ ws, KOut o) {
+  static_assert(!FTM || BG != 0, "on-chip messages: compile-time schedules only");
   using F = FOps<PREC>;
   constexpr int LANES = F::lanes;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -151,8 +180,24 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
   const uint32_t zl = (uint32_t)z * 4u;
   const long long n_c = (long long)p.n_blocks * p.z;
   uint8_t* Lg = smem + data_off + (uint32_t)g * p.l_bytes;
-  uint32_t* Mg = ws + gg * (long long)p.n_edges * p.z + z;  // edge e at Mg[e * Z]
+  // edge e at Mg[e * Z]; FTM: only the global rows' e_reg edges have workspace
+  uint32_t* Mg = ws + gg * (long long)(FTM ? p.e_reg : p.n_edges) * p.z + z;
   FltState& gs = gstate[g];
+  // FTM: shared message rows after L (one group), tensor-memory slot
+  const uint32_t Ms = (uint32_t)__cvta_generic_to_shared(Lg + p.l_bytes) + (uint32_t)z * p.m_stride;
+  uint32_t tbase = 0;
+  if constexpr (FTM) {
+    if (tid < 32) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(&cta->kc[5])));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const int warp = tid >> 5;
+    tbase = lds_u32(&cta->kc[5]) + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * p.tm_slot;
+  }
 
   if (tid == 0) {
     const long long first = (long long)blockIdx.x * p.groups * LANES;
@@ -188,8 +233,17 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
       }
       *reinterpret_cast<uint32_t*>(Lg + (uint32_t)n * 4u) = v;
     }
-    if (active)
+    if constexpr (FTM) {
+      for (int e = 0; e < p.e_reg; ++e) Mg[(long long)e * p.z] = 0u;  // the global rows come first
+      uint4* m4 = reinterpret_cast<uint4*>(Lg + p.l_bytes);
+      for (uint32_t k = z; k < (p.m_bytes >> 4); k += p.z) m4[k] = make_uint4(0u, 0u, 0u, 0u);
+      uint32_t c = 0;
+      for (; c + 4 <= p.tm_cols; c += 4) tm_st4(tbase + c, 0u, 0u, 0u, 0u);
+      for (; c < p.tm_cols; ++c) tm_st1(tbase + c, 0u);
+      tm_wait_st();
+    } else if (active) {
       for (int e = 0; e < p.n_edges; ++e) Mg[(long long)e * p.z] = 0u;
+    }
   }
   __syncthreads();
 
@@ -204,15 +258,15 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
       const uint4 B = p.unit_b[u];
       dispatch_unit<BG, 0>(A.x, [&](auto WA, auto WB) {
         constexpr int wa = decltype(WA)::value, wb = decltype(WB)::value;
-        FRow<PREC, wa> ra;
-        ra.pro(p, A.z, A.w, zl, ZL, Mg, active);
+        FRow<PREC, wa, FTM ? ftm_kind<BG>(wa) : 0> ra;
+        ra.pro(p, A.z, A.w, zl, ZL, Mg, active, Ms, tbase);
         if constexpr (wb == 0) {
           if (bar_prev) __syncthreads();
           ra.main(Lg, beta);
           ra.scatter(Lg, p, active);
         } else {
-          FRow<PREC, wb> rb;
-          rb.pro(p, B.x, B.y, zl, ZL, Mg, active);
+          FRow<PREC, wb, FTM ? ftm_kind<BG>(wb) : 0> rb;
+          rb.pro(p, B.x, B.y, zl, ZL, Mg, active, Ms, tbase);
           if (bar_prev) __syncthreads();
           ra.main(Lg, beta);
           rb.main(Lg, beta);
@@ -223,6 +277,7 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
       bar_prev = A.y != 0;
     }
     if (bar_prev) __syncthreads();
+    if constexpr (FTM) tm_wait_st();  // the next iteration reads these messages back
    } else {
     for (int r = 0; r < p.rows; ++r) {
       const int e0 = p.row_start[r];
@@ -381,6 +436,12 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
     }
     __syncthreads();
     if (__syncthreads_and(!p.trace && cta->n_done >= cta->n_valid)) break;
+  }
+  if constexpr (FTM) {
+    tm_wait_st();
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(lds_u32(&cta->kc[5])));
   }
 }
 
