@@ -612,3 +612,32 @@ def test_multi_device_decoder_matches_single_decode(cuda_ok, bg_id, z, stop, bat
     assert np.array_equal(res.syndrome_weight, ref.syndrome_weight) and np.array_equal(res.success, ref.success)
     if stop == "crc":
         assert np.array_equal(res.crc_ok, ref.crc_ok)
+
+
+@pytest.mark.parametrize("prec,bg_id,z,rows,stop,batch", [
+    ("f16", "BG1", 384, 46, "none", 33), ("f32", "BG1", 384, 46, "syndrome", 17),
+    ("f16", "BG2", 384, 42, "syndrome", 40), ("f32", "BG2", 256, 20, "none", 9),
+    ("f16", "BG1", 288, 9, "none", 5), ("f16", "BG1", 384, 4, "syndrome", 4)])
+def test_float_on_chip_messages_match_workspace_and_oracle(cuda_ok, prec, bg_id, z, rows, stop, batch, monkeypatch):
+    """Single-group BG1/BG2 float shapes keep their messages on chip (shared
+    and tensor memory; BG1 core rows in the workspace); NRLDPC_NO_TM=1 keeps
+    them all in the global workspace. Both must give the oracle's results."""
+    bg = nr.load_basegraph(bg_id, z)
+    params = nr.code_params(bg, z, rows)
+    _, llr = noisy_llrs(bg, rows, 1.5, batch, seed=(z, rows, 5))
+    blocks = nr.quantize(llr, nr.QuantConfig(mode=prec), params)
+    cfg = nr.DecodeConfig(max_iter=7, early_stop=stop, precision=prec)
+    ref = oracle.decode(blocks, bg, cfg)
+    smem = []
+    for no_tm in (False, True):
+        if no_tm:
+            monkeypatch.setenv("NRLDPC_NO_TM", "1")
+        plan = nr.Plan(bg, rows, cfg)
+        smem.append(plan.smem_bytes)
+        out = plan.alloc_outputs(batch)
+        plan.decode_device(torch.from_numpy(blocks).cuda(), out)
+        torch.cuda.synchronize()
+        assert np.array_equal(nr.unpack_bits(out["bits"].cpu().numpy(), params.k), ref["bits"])
+        assert np.array_equal(out["iters"].cpu().numpy(), ref["iterations"])
+        assert np.array_equal(out["synd"].cpu().numpy(), ref["syndrome_weight"])
+    assert smem[0] != smem[1]
