@@ -641,3 +641,38 @@ def test_float_on_chip_messages_match_workspace_and_oracle(cuda_ok, prec, bg_id,
         assert np.array_equal(out["iters"].cpu().numpy(), ref["iterations"])
         assert np.array_equal(out["synd"].cpu().numpy(), ref["syndrome_weight"])
     assert smem[0] != smem[1]
+
+
+def test_tm_plans_concurrent_with_each_other_and_cublas(cuda_ok):
+    """TM-layout kernels allocate all 512 tensor-memory columns of their SM.
+    Several TM plans on concurrent streams, next to cuBLAS GEMMs (which use
+    tensor memory on sm_100) on another stream, must neither deadlock nor
+    change results."""
+    cases = [("BG1", 384, 46), ("BG2", 384, 42), ("BG1", 256, 46), ("BG1", 320, 30)]
+    plans, blocks, refs, outs = [], [], [], []
+    for bg_id, z, rows in cases:
+        bg = nr.load_basegraph(bg_id, z)
+        cfg = nr.DecodeConfig(max_iter=6, early_stop="syndrome")
+        _, llr = noisy_llrs(bg, rows, 1.5, 150, seed=(z, rows, 3))
+        b = oracle.quantize_i8(llr, z)
+        plans.append(nr.Plan(bg, rows, cfg))
+        blocks.append(torch.from_numpy(b).cuda())
+        refs.append(oracle.decode(b, bg, cfg))
+        outs.append([plans[-1].alloc_outputs(150) for _ in range(3)])
+    streams = [torch.cuda.Stream() for _ in range(len(cases))]
+    gemm_stream = torch.cuda.Stream()
+    a = torch.randn(4096, 4096, device="cuda", dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(gemm_stream):
+        for _ in range(8):
+            a = (a @ a).clamp_(-1, 1)
+    for rep in range(3):
+        for i, plan in enumerate(plans):
+            plan.decode_device(blocks[i], outs[i][rep], stream=streams[i].cuda_stream)
+    torch.cuda.synchronize()
+    for i, (bg_id, z, rows) in enumerate(cases):
+        k = nr.code_params(nr.load_basegraph(bg_id, z), z, rows).k
+        for rep in range(3):
+            o = outs[i][rep]
+            assert np.array_equal(nr.unpack_bits(o["bits"].cpu().numpy(), k), refs[i]["bits"])
+            assert np.array_equal(o["iters"].cpu().numpy(), refs[i]["iterations"])
