@@ -411,7 +411,17 @@ __host__ __device__ constexpr int tm_smw() {
   return BG == 2 ? 8 : NREG == 6 ? 7 : 11;
 }
 
-template <int MAXW, bool REGMSG, int SMW = 7>
+// Rows whose last edge is their degree-1 extension column, with shift 0 in
+// every lifting (TS 38.212 base graphs: BG1 rows >= 4, BG2 rows >= 4; the
+// host checks the tables, tm_shape). Told apart by weight: the core rows are
+// the only ones of weight 19 (BG1) or 8 and 10 (BG2). Thread z's position in
+// that column is z itself, so its address needs no modular arithmetic.
+template <int BG>
+__host__ __device__ constexpr bool tm_diag(int w) {
+  return BG == 1 ? w != 19 : w <= 6;
+}
+
+template <int MAXW, bool REGMSG, int SMW = 7, bool DIAG = false>
 struct RowWorkTM {
   static constexpr bool TMEM = !REGMSG && MAXW < SMW;
   uint32_t off[MAXW];
@@ -436,7 +446,8 @@ struct RowWorkTM {
       for (int j = 0; j < MAXW; ++j) mw[j] = lds_u32(Ma + 4 * j);
     }
 #pragma unroll
-    for (int j = 0; j < MAXW; ++j) off[j] = edge_offset(tsh[j], tcb[j], zl, ZL);
+    for (int j = 0; j < MAXW; ++j)
+      off[j] = DIAG && j == MAXW - 1 ? zl + tcb[j] : edge_offset(tsh[j], tcb[j], zl, ZL);
   }
   __device__ __forceinline__ void gather_main(const uint32_t* mreg, uint32_t magic) {
     if constexpr (TMEM) tm_wait_ld<MAXW>(mw);
@@ -487,10 +498,10 @@ struct TmCtx {
   Consts k;
 };
 
-template <int W, bool REGMSG, int SMW>
+template <int W, bool REGMSG, int SMW, bool DIAG>
 __device__ __forceinline__ void process_row_tm(const KParams& p, uint32_t tb, uint32_t mb, const TmCtx& c,
                                                uint32_t* mreg, bool bar) {
-  RowWorkTM<W, REGMSG, SMW> r;
+  RowWorkTM<W, REGMSG, SMW, DIAG> r;
   r.gather_pro(p, tb, mb, c.zl, c.ZL, c.Ms, c.tbase);
   if (bar) __syncthreads();
   r.gather_main(mreg, c.k.magic);
@@ -498,11 +509,11 @@ __device__ __forceinline__ void process_row_tm(const KParams& p, uint32_t tb, ui
   r.scatter(mreg, c.k.one);
 }
 
-template <int WA, int WB, int SMW>
+template <int WA, int WB, int SMW, bool DIAG>
 __device__ __forceinline__ void process_rows2_tm(const KParams& p, uint32_t tba, uint32_t mba, uint32_t tbb,
                                                  uint32_t mbb, const TmCtx& c, bool bar) {
-  RowWorkTM<WA, false, SMW> a;
-  RowWorkTM<WB, false, SMW> b;
+  RowWorkTM<WA, false, SMW, DIAG> a;
+  RowWorkTM<WB, false, SMW, DIAG> b;
   a.gather_pro(p, tba, mba, c.zl, c.ZL, c.Ms, c.tbase);
   b.gather_pro(p, tbb, mbb, c.zl, c.ZL, c.Ms, c.tbase);
   if (bar) __syncthreads();
@@ -514,14 +525,15 @@ __device__ __forceinline__ void process_rows2_tm(const KParams& p, uint32_t tba,
   b.scatter(nullptr, c.k.one);
 }
 
-template <int MAXW>
+template <int MAXW, bool DIAG>
 __device__ __forceinline__ void row_parity_tm(const KParams& p, const uint32_t tb, uint32_t zl, uint32_t ZL,
                                               int& wa, int& wb) {
   uint32_t tsh[MAXW], tcb[MAXW];
   load_row_tables<MAXW>(p, tb, MAXW, tsh, tcb);
   uint32_t x = 0;
 #pragma unroll
-  for (int j = 0; j < MAXW; ++j) x ^= lds_u32(edge_offset(tsh[j], tcb[j], zl, ZL));
+  for (int j = 0; j < MAXW; ++j)
+    x ^= lds_u32(DIAG && j == MAXW - 1 ? zl + tcb[j] : edge_offset(tsh[j], tcb[j], zl, ZL));
   // bit 7 of each half's low byte is 1 for a non-negative value
   if (MAXW & 1) x ^= 0x00800080u;
   wa += (x >> 7) & 1u;
@@ -787,12 +799,12 @@ __device__ __forceinline__ void one_iteration_tm(const KParams& p, const TmCtx& 
   if constexpr (NREG == 6) {
 #pragma unroll 1
     for (int r = 0; r < 4; r += 2) {
-      process_row_tm<19, true, SMW>(p, 5u * r, 0, c, rm.q[0], r != 0);
-      process_row_tm<19, true, SMW>(p, 5u * r + 5u, 0, c, rm.q[1], true);
+      process_row_tm<19, true, SMW, false>(p, 5u * r, 0, c, rm.q[0], r != 0);
+      process_row_tm<19, true, SMW, false>(p, 5u * r + 5u, 0, c, rm.q[1], true);
       rm.rotate2();
     }
-    process_row_tm<3, true, SMW>(p, 20u, 0, c, rm.r4, true);
-    process_row_tm<8, true, SMW>(p, 21u, 0, c, rm.r5, true);
+    process_row_tm<3, true, SMW, tm_diag<BG>(3)>(p, 20u, 0, c, rm.r4, true);
+    process_row_tm<8, true, SMW, tm_diag<BG>(8)>(p, 21u, 0, c, rm.r5, true);
     bar_prev = true;
   }
   uint32_t ncode = p.unit_a[0].x;
@@ -804,8 +816,8 @@ __device__ __forceinline__ void one_iteration_tm(const KParams& p, const TmCtx& 
     ncode = p.unit_a[u + 1].x;
     dispatch_unit<BG, NREG>(code, [&](auto WA, auto WB) {
       constexpr int wa = decltype(WA)::value, wb = decltype(WB)::value;
-      if constexpr (wb == 0) process_row_tm<wa, false, SMW>(p, A.z, A.w, c, nullptr, bar_prev);
-      else process_rows2_tm<wa, wb, SMW>(p, A.z, A.w, B.x, B.y, c, bar_prev);
+      if constexpr (wb == 0) process_row_tm<wa, false, SMW, tm_diag<BG>(wa)>(p, A.z, A.w, c, nullptr, bar_prev);
+      else process_rows2_tm<wa, wb, SMW, tm_diag<BG>(wa) && tm_diag<BG>(wb)>(p, A.z, A.w, B.x, B.y, c, bar_prev);
     });
     bar_prev = A.y != 0;
   }
@@ -825,7 +837,10 @@ __device__ __forceinline__ void local_check_tm(const KParams& p, uint32_t zl, ui
     const int e0 = p.row_start[r];
     const int t0 = p.tab_start[r];
     const int w = p.row_start[r + 1] - e0;
-    dispatch_w<BG>(w, [&](auto W) { row_parity_tm<decltype(W)::value>(p, t0 / 4u, zl, ZL, wa, wb); });
+    dispatch_w<BG>(w, [&](auto W) {
+      constexpr int wv = decltype(W)::value;
+      row_parity_tm<wv, tm_diag<BG>(wv)>(p, t0 / 4u, zl, ZL, wa, wb);
+    });
     if (early) {
       const bool fa = !need_a || __any_sync(0xFFFFFFFFu, wa != 0);
       const bool fb = !need_b || __any_sync(0xFFFFFFFFu, wb != 0);
@@ -2147,6 +2162,13 @@ Shape tm_shape(const nrldpc_plan* p, const Shape& leg) {
   const int warps = p->z / 32;
   const uint32_t slot = 512u / (uint32_t)((warps + 3) / 4);
   const KParams& b = p->base;
+  // the row bodies take the last edge of every non-core row as the degree-1
+  // extension column at shift 0 (tm_diag)
+  for (int r = 0; r < p->rows; ++r) {
+    const int w = b.row_start[r + 1] - b.row_start[r];
+    const bool diag = p->schedule == 1 ? tm_diag<1>(w) : tm_diag<2>(w);
+    if (diag && b.sh[b.tab_start[r] + w - 1] != 0) return leg;
+  }
   MsgLayout ml{};
   uint32_t sm_slots = 0, tm_cols = 0;
   for (int r = leg.nreg; r < p->rows; ++r) {
