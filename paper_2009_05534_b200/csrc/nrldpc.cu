@@ -819,8 +819,10 @@ __device__ __forceinline__ void one_iteration_tm(const KParams& p, const TmCtx& 
       process_row_tm<19, true, SMW, false>(p, 5u * r + 5u, 0, c, rm.q[1], true);
       rm.rotate2();
     }
-    process_row_tm<3, true, SMW, tm_diag<BG>(3)>(p, 20u, 0, c, rm.r4, true);
-    process_row_tm<8, true, SMW, tm_diag<BG>(8)>(p, 21u, 0, c, rm.r5, true);
+    // rows 4 and 5 keep their messages in tensor memory (SMW 9: both weights
+    // below it), so their byte-pair registers and PRMTs go away
+    process_row_tm<3, false, 9, tm_diag<BG>(3)>(p, 20u, p.tm_r45[0], c, nullptr, true);
+    process_row_tm<8, false, 9, tm_diag<BG>(8)>(p, 21u, p.tm_r45[1], c, nullptr, true);
     bar_prev = true;
   }
   uint32_t ncode = p.unit_a[0].x;
@@ -2187,6 +2189,12 @@ Shape tm_shape(const nrldpc_plan* p, const Shape& leg) {
   }
   MsgLayout ml{};
   uint32_t sm_slots = 0, tm_cols = 0;
+  uint32_t r45[2] = {0, 0};
+  if (leg.nreg == 6) {  // rows 4 and 5: tensor memory (one_iteration_tm)
+    r45[0] = 0;
+    r45[1] = (uint32_t)(b.row_start[5] - b.row_start[4]);
+    tm_cols = (uint32_t)(b.row_start[6] - b.row_start[4]);
+  }
   for (int r = leg.nreg; r < p->rows; ++r) {
     const int w = b.row_start[r + 1] - b.row_start[r];
     if (w >= smw) {
@@ -2217,6 +2225,8 @@ Shape tm_shape(const nrldpc_plan* p, const Shape& leg) {
   sh.kp.m_stride = e * 4u;
   sh.kp.tm_cols = tm_cols;
   sh.kp.tm_slot = slot;
+  sh.kp.tm_r45[0] = r45[0];
+  sh.kp.tm_r45[1] = r45[1];
   build_units(p, leg.nreg, ml, sh.kp);
   for (int t = 0; t < NR_MAX_TAB; ++t) {
     sh.kp.sh[t] = b.sh[t] * 4u;

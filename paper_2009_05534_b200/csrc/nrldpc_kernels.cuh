@@ -57,6 +57,7 @@ struct alignas(16) KParams {
   uint32_t abs_base; // nonzero: cb holds shared-window addresses, L starts here
   uint32_t tm_cols;  // TM layout: tensor-memory message columns per thread
   uint32_t tm_slot;  // TM layout: columns per thread slot (512 / warps per lane quarter, rounded down)
+  uint32_t tm_r45[2];  // TM layout, register-row shapes: TMEM columns of rows 4 and 5
   uint16_t row_start[NR_MAX_ROWS + 1];  // first edge of each row (message offsets)
   uint16_t tab_start[NR_MAX_ROWS + 1];  // row's first slot in sh/cb (multiple of 4)
   uint8_t bar_after[NR_MAX_ROWS];       // 0: next row is column-disjoint from this layer
