@@ -844,12 +844,25 @@ __device__ __forceinline__ void one_iteration_tm(const KParams& p, const TmCtx& 
   tm_wait_st();
 }
 
-// local_check for the TM layout (Z % 32 == 0, one group)
+// min |L| over this thread's positions of both lanes (decoder.py:480-483)
+__device__ __forceinline__ void margin_tm(const KParams& p, uint32_t zl, uint32_t ZL, uint32_t Ls, int* mabs) {
+  int ma = 255, mb = 255;
+  for (int c = 0; c < p.n_blocks; ++c) {
+    const uint32_t u = lds_u32(Ls + (uint32_t)c * ZL + zl);
+    ma = min(ma, abs((int)(u & 0xFFu) - 128));
+    mb = min(mb, abs((int)((u >> 16) & 0xFFu) - 128));
+  }
+  mabs[0] = ma;
+  mabs[1] = mb;
+}
+
+// local_check for the TM layout (Z % 32 == 0, one group). In early mode the
+// margin (min |L|) is left out (mabs = 255): it only matters for a lane whose
+// syndrome is zero, and the caller computes it in a second pass only then.
 template <int BG>
 __device__ __forceinline__ void local_check_tm(const KParams& p, uint32_t zl, uint32_t ZL, uint32_t Ls, int* wcnt,
                                                int* mabs, bool early, bool need_a, bool need_b) {
   int wa = 0, wb = 0;
-  bool stopped = false;
 #pragma unroll 1
   for (int r = 0; r < p.rows; ++r) {
     const int e0 = p.row_start[r];
@@ -862,22 +875,13 @@ __device__ __forceinline__ void local_check_tm(const KParams& p, uint32_t zl, ui
     if (early) {
       const bool fa = !need_a || __any_sync(0xFFFFFFFFu, wa != 0);
       const bool fb = !need_b || __any_sync(0xFFFFFFFFu, wb != 0);
-      if (fa && fb) {
-        stopped = true;
-        break;
-      }
+      if (fa && fb) break;
     }
   }
-  int ma = 255, mb = 255;
-  for (int c = 0; c < p.n_blocks && !stopped; ++c) {
-    const uint32_t u = lds_u32(Ls + (uint32_t)c * ZL + zl);
-    ma = min(ma, abs((int)(u & 0xFFu) - 128));
-    mb = min(mb, abs((int)((u >> 16) & 0xFFu) - 128));
-  }
+  mabs[0] = mabs[1] = 255;
+  if (!early) margin_tm(p, zl, ZL, Ls, mabs);
   wcnt[0] = wa;
   wcnt[1] = wb;
-  mabs[0] = ma;
-  mabs[1] = mb;
 }
 
 // early: only "any unsatisfied check" matters (an early-stop iteration that
@@ -1179,10 +1183,10 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
     if (!(p.early_stop != NRLDPC_STOP_NONE || p.trace || last)) continue;
 
     // ---- end-of-iteration check (decoder.py:497-536) ----
+    // weights are only needed in full when traced or final
+    const bool early = BG != 0 && !p.trace && !last && p.z % 32 == 0;
     {
       int wc[2], ma[2];
-      // weights are only needed in full when traced or final
-      const bool early = BG != 0 && !p.trace && !last && p.z % 32 == 0;
       if constexpr (TM)
         local_check_tm<BG>(p, zl, ZL, p.abs_base, wc, ma, early, lane_valid[0] && !gs.done[0],
                        lane_valid[1] && !gs.done[1]);
@@ -1198,6 +1202,18 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
       }
     }
     __syncthreads();
+    if constexpr (TM) {
+      // second pass: the margin, only when a live lane's syndrome is zero
+      // (block-uniform: shared state read after the barrier)
+      if (early && ((lane_valid[0] && !gs.done[0] && gs.synd[0] == 0) ||
+                    (lane_valid[1] && !gs.done[1] && gs.synd[1] == 0))) {
+        int ma[2];
+        margin_tm(p, zl, ZL, p.abs_base, ma);
+        atomicMin(&gs.minabs[0], ma[0]);
+        atomicMin(&gs.minabs[1], ma[1]);
+        __syncthreads();
+      }
+    }
     int cand[2] = {0, 0};
     if (active && p.early_stop != NRLDPC_STOP_NONE) {
 #pragma unroll
@@ -1475,6 +1491,16 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const 
       }
     }
     __syncthreads();
+    if constexpr (TM) {
+      // second pass: the margin, only when a live lane's syndrome is zero
+      if (!last[0] && !last[1] && ((act[0] && gs.synd[0] == 0) || (act[1] && gs.synd[1] == 0))) {
+        int ma[2];
+        margin_tm(p, zl, ZL, p.abs_base, ma);
+        atomicMin(&gs.minabs[0], ma[0]);
+        atomicMin(&gs.minabs[1], ma[1]);
+        __syncthreads();
+      }
+    }
     int cand[2], fin[2];
 #pragma unroll
     for (int l = 0; l < 2; ++l) cand[l] = act[l] && gs.synd[l] == 0 && gs.minabs[l] > 0;
