@@ -856,13 +856,21 @@ __device__ __forceinline__ void margin_tm(const KParams& p, uint32_t zl, uint32_
   mabs[1] = mb;
 }
 
-// local_check for the TM layout (Z % 32 == 0, one group). In early mode the
-// margin (min |L|) is left out (mabs = 255): it only matters for a lane whose
-// syndrome is zero, and the caller computes it in a second pass only then.
+// local_check for the TM layout (Z % 32 == 0, one group). Early mode (an
+// early-stop iteration that is neither traced nor final) needs only "does
+// any check fail" per lane, so the warps cooperate: a warp that holds a
+// failing check of a live lane publishes it at once in the group's syndrome
+// counter (synd), and every warp stops scanning rows as soon as the counters
+// show a failure for every live lane. wcnt then returns 0 (already counted),
+// and the margin (min |L|) is left out (mabs = 255): it only matters for a
+// lane whose syndrome is zero, and the caller computes it in a second pass
+// only then.
 template <int BG>
 __device__ __forceinline__ void local_check_tm(const KParams& p, uint32_t zl, uint32_t ZL, uint32_t Ls, int* wcnt,
-                                               int* mabs, bool early, bool need_a, bool need_b) {
+                                               int* mabs, bool early, bool need_a, bool need_b, int* synd) {
   int wa = 0, wb = 0;
+  bool pub_a = !need_a, pub_b = !need_b;  // nothing to publish for a lane not being decoded
+  const bool leader = (threadIdx.x & 31) == 0;
 #pragma unroll 1
   for (int r = 0; r < p.rows; ++r) {
     const int e0 = p.row_start[r];
@@ -873,15 +881,26 @@ __device__ __forceinline__ void local_check_tm(const KParams& p, uint32_t zl, ui
       row_parity_tm<wv, tm_diag<BG>(wv)>(p, t0 / 4u, zl, ZL, wa, wb);
     });
     if (early) {
-      const bool fa = !need_a || __any_sync(0xFFFFFFFFu, wa != 0);
-      const bool fb = !need_b || __any_sync(0xFFFFFFFFu, wb != 0);
-      if (fa && fb) break;
+      if (!pub_a && __any_sync(0xFFFFFFFFu, wa != 0)) {
+        if (leader) atomicAdd(&synd[0], 1);
+        pub_a = true;
+      }
+      if (!pub_b && __any_sync(0xFFFFFFFFu, wb != 0)) {
+        if (leader) atomicAdd(&synd[1], 1);
+        pub_b = true;
+      }
+      const volatile int* vs = synd;
+      if ((!need_a || vs[0] != 0) && (!need_b || vs[1] != 0)) break;
     }
   }
   mabs[0] = mabs[1] = 255;
-  if (!early) margin_tm(p, zl, ZL, Ls, mabs);
-  wcnt[0] = wa;
-  wcnt[1] = wb;
+  if (early) {
+    wcnt[0] = wcnt[1] = 0;
+  } else {
+    margin_tm(p, zl, ZL, Ls, mabs);
+    wcnt[0] = wa;
+    wcnt[1] = wb;
+  }
 }
 
 // early: only "any unsatisfied check" matters (an early-stop iteration that
@@ -1189,7 +1208,7 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
       int wc[2], ma[2];
       if constexpr (TM)
         local_check_tm<BG>(p, zl, ZL, p.abs_base, wc, ma, early, lane_valid[0] && !gs.done[0],
-                       lane_valid[1] && !gs.done[1]);
+                           lane_valid[1] && !gs.done[1], gs.synd);
       else
         local_check<BG, MAXW, LANES, ABS>(p, zl, ZL, Lg, wc, ma, early, lane_valid[0] && !gs.done[0],
                                           lane_valid[1] && !gs.done[1]);
@@ -1482,7 +1501,7 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const 
     }
     {
       int wc[2], ma[2];
-      if constexpr (TM) local_check_tm<BG>(p, zl, ZL, p.abs_base, wc, ma, !last[0] && !last[1], act[0], act[1]);
+      if constexpr (TM) local_check_tm<BG>(p, zl, ZL, p.abs_base, wc, ma, !last[0] && !last[1], act[0], act[1], gs.synd);
       else local_check<BG, MAXW, LANES, ABS>(p, zl, ZL, Lg, wc, ma, !last[0] && !last[1], act[0], act[1]);
 #pragma unroll
       for (int l = 0; l < 2; ++l) {
