@@ -845,15 +845,45 @@ __device__ __forceinline__ void one_iteration_tm(const KParams& p, const TmCtx& 
 }
 
 // min |L| over this thread's positions of both lanes (decoder.py:480-483)
+// (four independent min chains, so the loads overlap)
 __device__ __forceinline__ void margin_tm(const KParams& p, uint32_t zl, uint32_t ZL, uint32_t Ls, int* mabs) {
-  int ma = 255, mb = 255;
-  for (int c = 0; c < p.n_blocks; ++c) {
-    const uint32_t u = lds_u32(Ls + (uint32_t)c * ZL + zl);
-    ma = min(ma, abs((int)(u & 0xFFu) - 128));
-    mb = min(mb, abs((int)((u >> 16) & 0xFFu) - 128));
+  int ma[4] = {255, 255, 255, 255}, mb[4] = {255, 255, 255, 255};
+  int c = 0;
+  for (; c + 4 <= p.n_blocks; c += 4) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t u = lds_u32(Ls + (uint32_t)(c + i) * ZL + zl);
+      ma[i] = min(ma[i], abs((int)(u & 0xFFu) - 128));
+      mb[i] = min(mb[i], abs((int)((u >> 16) & 0xFFu) - 128));
+    }
   }
-  mabs[0] = ma;
-  mabs[1] = mb;
+  for (; c < p.n_blocks; ++c) {
+    const uint32_t u = lds_u32(Ls + (uint32_t)c * ZL + zl);
+    ma[0] = min(ma[0], abs((int)(u & 0xFFu) - 128));
+    mb[0] = min(mb[0], abs((int)((u >> 16) & 0xFFu) - 128));
+  }
+  mabs[0] = min(min(ma[0], ma[1]), min(ma[2], ma[3]));
+  mabs[1] = min(min(mb[0], mb[1]), min(mb[2], mb[3]));
+}
+
+// Table slot quad of row R in the compile-time schedules (rows padded to 4
+// slots; host: nrldpc_plan_create's table builder).
+template <int BG, int R>
+__host__ __device__ constexpr uint32_t row_tq() {
+  uint32_t t = 0;
+  for (int r = 0; r < R; ++r) t += (uint32_t)(RowW<BG>::w[r] + 3) / 4u;
+  return t;
+}
+
+// Full syndrome of a full compile-time graph as one straight-line block (no
+// per-row dispatch), so the loads of many rows are in flight together.
+template <int BG, int R = 0>
+__device__ __forceinline__ void parity_rows_tm(const KParams& p, uint32_t zl, uint32_t ZL, int& wa, int& wb) {
+  if constexpr (R < RowW<BG>::n) {
+    constexpr int w = RowW<BG>::w[R];
+    row_parity_tm<w, tm_diag<BG>(w)>(p, row_tq<BG, R>(), zl, ZL, wa, wb);
+    parity_rows_tm<BG, R + 1>(p, zl, ZL, wa, wb);
+  }
 }
 
 // local_check for the TM layout (Z % 32 == 0, one group). Early mode (an
@@ -871,6 +901,14 @@ __device__ __forceinline__ void local_check_tm(const KParams& p, uint32_t zl, ui
   int wa = 0, wb = 0;
   bool pub_a = !need_a, pub_b = !need_b;  // nothing to publish for a lane not being decoded
   const bool leader = (threadIdx.x & 31) == 0;
+  if (!early && p.rows == RowW<BG>::n) {
+    parity_rows_tm<BG>(p, zl, ZL, wa, wb);
+    mabs[0] = mabs[1] = 255;
+    margin_tm(p, zl, ZL, Ls, mabs);
+    wcnt[0] = wa;
+    wcnt[1] = wb;
+    return;
+  }
 #pragma unroll 1
   for (int r = 0; r < p.rows; ++r) {
     const int e0 = p.row_start[r];
