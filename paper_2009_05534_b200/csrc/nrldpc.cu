@@ -845,25 +845,23 @@ __device__ __forceinline__ void one_iteration_tm(const KParams& p, const TmCtx& 
 }
 
 // min |L| over this thread's positions of both lanes (decoder.py:480-483)
-// (four independent min chains, so the loads overlap)
+// (four independent min chains, so the loads overlap; the posteriors are
+// the biased half2 {1152+v_a, 1152+v_b}, so |v| is one HADD2 plus the |.|
+// operand of HMNMX2 for both lanes)
 __device__ __forceinline__ void margin_tm(const KParams& p, uint32_t zl, uint32_t ZL, uint32_t Ls, int* mabs) {
-  int ma[4] = {255, 255, 255, 255}, mb[4] = {255, 255, 255, 255};
+  const half2 H255 = u2h(0x5BF85BF8u), H1152 = u2h(0x64806480u);
+  half2 acc[4] = {H255, H255, H255, H255};
   int c = 0;
   for (; c + 4 <= p.n_blocks; c += 4) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t u = lds_u32(Ls + (uint32_t)(c + i) * ZL + zl);
-      ma[i] = min(ma[i], abs((int)(u & 0xFFu) - 128));
-      mb[i] = min(mb[i], abs((int)((u >> 16) & 0xFFu) - 128));
-    }
+    for (int i = 0; i < 4; ++i)
+      acc[i] = __hmin2(acc[i], __habs2(__hsub2(u2h(lds_u32(Ls + (uint32_t)(c + i) * ZL + zl)), H1152)));
   }
-  for (; c < p.n_blocks; ++c) {
-    const uint32_t u = lds_u32(Ls + (uint32_t)c * ZL + zl);
-    ma[0] = min(ma[0], abs((int)(u & 0xFFu) - 128));
-    mb[0] = min(mb[0], abs((int)((u >> 16) & 0xFFu) - 128));
-  }
-  mabs[0] = min(min(ma[0], ma[1]), min(ma[2], ma[3]));
-  mabs[1] = min(min(mb[0], mb[1]), min(mb[2], mb[3]));
+  for (; c < p.n_blocks; ++c)
+    acc[0] = __hmin2(acc[0], __habs2(__hsub2(u2h(lds_u32(Ls + (uint32_t)c * ZL + zl)), H1152)));
+  const half2 m = __hmin2(__hmin2(acc[0], acc[1]), __hmin2(acc[2], acc[3]));
+  mabs[0] = (int)__low2float(m);   // exact small integers
+  mabs[1] = (int)__high2float(m);
 }
 
 // Table slot quad of row R in the compile-time schedules (rows padded to 4
