@@ -873,14 +873,40 @@ __host__ __device__ constexpr uint32_t row_tq() {
   return t;
 }
 
-// Full syndrome of a full compile-time graph as one straight-line block (no
-// per-row dispatch), so the loads of many rows are in flight together.
-template <int BG, int R = 0>
+// Full syndrome of a full compile-time graph (rows R..E-1) as one
+// straight-line block (no per-row dispatch), so the loads of many rows are in
+// flight together.
+template <int BG, int R = 0, int E = RowW<BG>::n>
 __device__ __forceinline__ void parity_rows_tm(const KParams& p, uint32_t zl, uint32_t ZL, int& wa, int& wb) {
-  if constexpr (R < RowW<BG>::n) {
+  if constexpr (R < E) {
     constexpr int w = RowW<BG>::w[R];
     row_parity_tm<w, tm_diag<BG>(w)>(p, row_tq<BG, R>(), zl, ZL, wa, wb);
-    parity_rows_tm<BG, R + 1>(p, zl, ZL, wa, wb);
+    parity_rows_tm<BG, R + 1, E>(p, zl, ZL, wa, wb);
+  }
+}
+
+// Early-mode scan of a full compile-time graph (see local_check_tm): blocks
+// of STEP straight-line rows, then publish this warp's failures and stop
+// once every live lane has one. Returns when done or stopped.
+template <int BG, int R, int STEP>
+__device__ __forceinline__ void parity_rows_early_tm(const KParams& p, uint32_t zl, uint32_t ZL, int& wa, int& wb,
+                                                     bool need_a, bool need_b, bool& pub_a, bool& pub_b,
+                                                     int* synd) {
+  if constexpr (R < RowW<BG>::n) {
+    constexpr int E = R + STEP < RowW<BG>::n ? R + STEP : RowW<BG>::n;
+    parity_rows_tm<BG, R, E>(p, zl, ZL, wa, wb);
+    const bool leader = (threadIdx.x & 31) == 0;
+    if (!pub_a && __any_sync(0xFFFFFFFFu, wa != 0)) {
+      if (leader) atomicAdd(&synd[0], 1);
+      pub_a = true;
+    }
+    if (!pub_b && __any_sync(0xFFFFFFFFu, wb != 0)) {
+      if (leader) atomicAdd(&synd[1], 1);
+      pub_b = true;
+    }
+    const volatile int* vs = synd;
+    if ((!need_a || vs[0] != 0) && (!need_b || vs[1] != 0)) return;
+    parity_rows_early_tm<BG, E, STEP>(p, zl, ZL, wa, wb, need_a, need_b, pub_a, pub_b, synd);
   }
 }
 
@@ -899,12 +925,17 @@ __device__ __forceinline__ void local_check_tm(const KParams& p, uint32_t zl, ui
   int wa = 0, wb = 0;
   bool pub_a = !need_a, pub_b = !need_b;  // nothing to publish for a lane not being decoded
   const bool leader = (threadIdx.x & 31) == 0;
-  if (!early && p.rows == RowW<BG>::n) {
-    parity_rows_tm<BG>(p, zl, ZL, wa, wb);
+  if (p.rows == RowW<BG>::n) {
     mabs[0] = mabs[1] = 255;
-    margin_tm(p, zl, ZL, Ls, mabs);
-    wcnt[0] = wa;
-    wcnt[1] = wb;
+    if (early) {
+      parity_rows_early_tm<BG, 0, 4>(p, zl, ZL, wa, wb, need_a, need_b, pub_a, pub_b, synd);
+      wcnt[0] = wcnt[1] = 0;
+    } else {
+      parity_rows_tm<BG>(p, zl, ZL, wa, wb);
+      margin_tm(p, zl, ZL, Ls, mabs);
+      wcnt[0] = wa;
+      wcnt[1] = wb;
+    }
     return;
   }
 #pragma unroll 1
