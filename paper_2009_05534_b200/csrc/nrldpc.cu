@@ -970,6 +970,18 @@ __device__ __forceinline__ void local_check_tm(const KParams& p, uint32_t zl, ui
   }
 }
 
+// The byte-pair layout's full-graph syndrome as straight-line code (see
+// parity_rows_tm).
+template <int BG, int LANES, bool ABS, int R = 0>
+__device__ __forceinline__ void parity_rows(const KParams& p, uint32_t zl, uint32_t ZL,
+                                            const uint8_t* __restrict__ Lg, int& wa, int& wb) {
+  if constexpr (R < RowW<BG>::n) {
+    constexpr int w = RowW<BG>::w[R];
+    row_parity<w, LANES, ABS>(p, row_tq<BG, R>(), w, zl, ZL, Lg, wa, wb);
+    parity_rows<BG, LANES, ABS, R + 1>(p, zl, ZL, Lg, wa, wb);
+  }
+}
+
 // early: only "any unsatisfied check" matters (an early-stop iteration that
 // is neither traced nor the last). A warp then stops scanning rows once it
 // holds a failing check of every lane still being decoded (need_a/need_b):
@@ -988,6 +1000,8 @@ __device__ __forceinline__ void local_check(const KParams& p, uint32_t zl, uint3
       const int e0 = p.row_start[r];
       row_parity<MAXW, LANES>(p, p.tab_start[r] / 4u, p.row_start[r + 1] - e0, zl, ZL, Lg, wa, wb);
     }
+  } else if (!early && p.rows == RowW<BG>::n) {
+    parity_rows<BG, LANES, ABS>(p, zl, ZL, Lg, wa, wb);  // full graph: straight-line
   } else {
 #pragma unroll 1
     for (int r = 0; r < p.rows; ++r) {
@@ -1006,16 +1020,27 @@ __device__ __forceinline__ void local_check(const KParams& p, uint32_t zl, uint3
       }
     }
   }
-  int ma = 255, mb = 255;
-  for (int c = 0; c < p.n_blocks && !stopped; ++c) {
-    const uint32_t u = ld_elem<LANES>(Lg + (uint32_t)c * ZL + zl);
-    ma = min(ma, abs((int)(u & 0xFFu) - 128));
-    mb = min(mb, abs((int)((u >> 8) & 0xFFu) - 128));
+  int ma[2] = {255, 255}, mb[2] = {255, 255};  // two chains, so the loads overlap
+  if (!stopped) {
+    int c = 0;
+    for (; c + 2 <= p.n_blocks; c += 2) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const uint32_t u = ld_elem<LANES>(Lg + (uint32_t)(c + i) * ZL + zl);
+        ma[i] = min(ma[i], abs((int)(u & 0xFFu) - 128));
+        mb[i] = min(mb[i], abs((int)((u >> 8) & 0xFFu) - 128));
+      }
+    }
+    if (c < p.n_blocks) {
+      const uint32_t u = ld_elem<LANES>(Lg + (uint32_t)c * ZL + zl);
+      ma[0] = min(ma[0], abs((int)(u & 0xFFu) - 128));
+      mb[0] = min(mb[0], abs((int)((u >> 8) & 0xFFu) - 128));
+    }
   }
   wcnt[0] = wa;
   wcnt[1] = wb;
-  mabs[0] = ma;
-  mabs[1] = mb;
+  mabs[0] = min(ma[0], ma[1]);
+  mabs[1] = min(mb[0], mb[1]);
 }
 
 // Hard decisions of the first K positions, bit-packed LSB-first
