@@ -150,6 +150,35 @@ struct FRow {
   }
 };
 
+// One row's parity of hard decisions (lvc < 0, -0 not negative) for the
+// end-of-iteration check, with the row weight known at compile time.
+template <int PREC, int W>
+__device__ __forceinline__ void flt_row_parity(const KParams& p, uint32_t tq, const uint8_t* Lg, uint32_t zl,
+                                               uint32_t ZL, int (&wc)[2]) {
+  using F = FOps<PREC>;
+  uint32_t tsh[W], tcb[W];
+  load_row_tables<W>(p, tq, W, tsh, tcb);
+  uint32_t par = 0;
+#pragma unroll
+  for (int j = 0; j < W; ++j) par ^= F::neg_mask(*reinterpret_cast<const uint32_t*>(Lg + edge_offset(tsh[j], tcb[j], zl, ZL)));
+  if (F::lanes == 1) {
+    wc[0] += par >> 31;
+  } else {  // half2 masks: lane 0 in bits 0-15, lane 1 in bits 16-31
+    wc[0] += (par >> 15) & 1u;
+    wc[1] += par >> 31;
+  }
+}
+
+// The full syndrome of a full compile-time graph as straight-line code.
+template <int PREC, int BG, int R = 0>
+__device__ __forceinline__ void flt_parity_rows(const KParams& p, const uint8_t* Lg, uint32_t zl, uint32_t ZL,
+                                                int (&wc)[2]) {
+  if constexpr (R < RowW<BG>::n) {
+    flt_row_parity<PREC, RowW<BG>::w[R]>(p, row_tq<BG, R>(), Lg, zl, ZL, wc);
+    flt_parity_rows<PREC, BG, R + 1>(p, Lg, zl, ZL, wc);
+  }
+}
+
 struct FltState {
   int synd[2];
   float minabs[2];
@@ -322,7 +351,14 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
     // end-of-iteration check (decoder.py:497-536)
     if (active) {
       int wc[2] = {0, 0};
-      for (int r = 0; r < p.rows; ++r) {
+      bool straight = false;
+      if constexpr (BG != 0) {
+        if (p.rows == RowW<BG>::n) {
+          flt_parity_rows<PREC, BG>(p, Lg, zl, ZL, wc);
+          straight = true;
+        }
+      }
+      for (int r = 0; r < p.rows && !straight; ++r) {
         const int w = p.row_start[r + 1] - p.row_start[r];
         uint32_t tsh[19], tcb[19];
         load_row_tables<19>(p, p.tab_start[r] / 4u, w, tsh, tcb);
