@@ -885,6 +885,18 @@ __device__ __forceinline__ void parity_rows_tm(const KParams& p, uint32_t zl, ui
   }
 }
 
+// The same for a partial graph (rows < p.rows): straight-line rows with a
+// uniform bound test before each.
+template <int BG, int R = 0>
+__device__ __forceinline__ void parity_rows_part_tm(const KParams& p, uint32_t zl, uint32_t ZL, int& wa, int& wb) {
+  if constexpr (R < RowW<BG>::n) {
+    if (R >= p.rows) return;
+    constexpr int w = RowW<BG>::w[R];
+    row_parity_tm<w, tm_diag<BG>(w)>(p, row_tq<BG, R>(), zl, ZL, wa, wb);
+    parity_rows_part_tm<BG, R + 1>(p, zl, ZL, wa, wb);
+  }
+}
+
 // Early-mode scan of a full compile-time graph (see local_check_tm): blocks
 // of STEP straight-line rows, then publish this warp's failures and stop
 // once every live lane has one. Returns when done or stopped.
@@ -938,6 +950,14 @@ __device__ __forceinline__ void local_check_tm(const KParams& p, uint32_t zl, ui
     }
     return;
   }
+  if (!early) {
+    parity_rows_part_tm<BG>(p, zl, ZL, wa, wb);
+    margin_tm(p, zl, ZL, Ls, mabs);
+    wcnt[0] = wa;
+    wcnt[1] = wb;
+    return;
+  }
+  // early mode, partial graph: row loop with the cooperative exit test
 #pragma unroll 1
   for (int r = 0; r < p.rows; ++r) {
     const int e0 = p.row_start[r];
@@ -947,27 +967,19 @@ __device__ __forceinline__ void local_check_tm(const KParams& p, uint32_t zl, ui
       constexpr int wv = decltype(W)::value;
       row_parity_tm<wv, tm_diag<BG>(wv)>(p, t0 / 4u, zl, ZL, wa, wb);
     });
-    if (early) {
-      if (!pub_a && __any_sync(0xFFFFFFFFu, wa != 0)) {
-        if (leader) atomicAdd(&synd[0], 1);
-        pub_a = true;
-      }
-      if (!pub_b && __any_sync(0xFFFFFFFFu, wb != 0)) {
-        if (leader) atomicAdd(&synd[1], 1);
-        pub_b = true;
-      }
-      const volatile int* vs = synd;
-      if ((!need_a || vs[0] != 0) && (!need_b || vs[1] != 0)) break;
+    if (!pub_a && __any_sync(0xFFFFFFFFu, wa != 0)) {
+      if (leader) atomicAdd(&synd[0], 1);
+      pub_a = true;
     }
+    if (!pub_b && __any_sync(0xFFFFFFFFu, wb != 0)) {
+      if (leader) atomicAdd(&synd[1], 1);
+      pub_b = true;
+    }
+    const volatile int* vs = synd;
+    if ((!need_a || vs[0] != 0) && (!need_b || vs[1] != 0)) break;
   }
   mabs[0] = mabs[1] = 255;
-  if (early) {
-    wcnt[0] = wcnt[1] = 0;
-  } else {
-    margin_tm(p, zl, ZL, Ls, mabs);
-    wcnt[0] = wa;
-    wcnt[1] = wb;
-  }
+  wcnt[0] = wcnt[1] = 0;
 }
 
 // The byte-pair layout's full-graph syndrome as straight-line code (see
