@@ -1,3 +1,10 @@
+#!/usr/bin/env python
+"""Single-launch and 1/2/3-stream overlapped batch time (ms per 1024-codeword
+batch, 10 fixed iterations) for BG2 Z=384, BG1 Z=256 and BG1 Z=384; run with
+and without NRLDPC_NO_TM=1 to compare the TM and byte-pair layouts.
+
+    python tools/ovl_probe.py
+"""
 import os, sys, json
 sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tools")
 import numpy as np, torch
