@@ -5,11 +5,18 @@ and without NRLDPC_NO_TM=1 to compare the TM and byte-pair layouts.
 
     python tools/ovl_probe.py
 """
-import os, sys, json
-sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tools")
-import numpy as np, torch
-import paper_2009_05534_b200 as nr
-from bench_configs import gpu_blocks, overlapped_ms, time_plan
+import json
+import os
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tools"))
+import numpy as np  # noqa: E402
+
+import paper_2009_05534_b200 as nr  # noqa: E402
+from bench_configs import gpu_blocks, overlapped_ms, time_plan  # noqa: E402
 res = {}
 for bgn, z in ((2, 384), (1, 256), (1, 384)):
     bg = nr.load_basegraph(bgn, z)
