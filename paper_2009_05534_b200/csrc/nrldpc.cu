@@ -984,13 +984,38 @@ __device__ __forceinline__ void local_check_tm(const KParams& p, uint32_t zl, ui
 
 // The byte-pair layout's full-graph syndrome as straight-line code (see
 // parity_rows_tm).
-template <int BG, int LANES, bool ABS, int R = 0>
+template <int BG, int LANES, bool ABS, int R = 0, int E = RowW<BG>::n>
 __device__ __forceinline__ void parity_rows(const KParams& p, uint32_t zl, uint32_t ZL,
                                             const uint8_t* __restrict__ Lg, int& wa, int& wb) {
-  if constexpr (R < RowW<BG>::n) {
+  if constexpr (R < E) {
     constexpr int w = RowW<BG>::w[R];
     row_parity<w, LANES, ABS>(p, row_tq<BG, R>(), w, zl, ZL, Lg, wa, wb);
-    parity_rows<BG, LANES, ABS, R + 1>(p, zl, ZL, Lg, wa, wb);
+    parity_rows<BG, LANES, ABS, R + 1, E>(p, zl, ZL, Lg, wa, wb);
+  }
+}
+
+// Early-mode scan of a full graph in the byte-pair layout: straight-line
+// blocks of STEP rows, then publish this warp's failures in the group's
+// counters and stop once every live lane has one (see local_check_tm).
+template <int BG, int LANES, bool ABS, int R, int STEP>
+__device__ __forceinline__ void parity_rows_early(const KParams& p, uint32_t zl, uint32_t ZL,
+                                                  const uint8_t* __restrict__ Lg, int& wa, int& wb, bool need_a,
+                                                  bool need_b, bool& pub_a, bool& pub_b, int* synd) {
+  if constexpr (R < RowW<BG>::n) {
+    constexpr int E = R + STEP < RowW<BG>::n ? R + STEP : RowW<BG>::n;
+    parity_rows<BG, LANES, ABS, R, E>(p, zl, ZL, Lg, wa, wb);
+    const bool leader = (threadIdx.x & 31) == 0;
+    if (!pub_a && __any_sync(0xFFFFFFFFu, wa != 0)) {
+      if (leader) atomicAdd(&synd[0], 1);
+      pub_a = true;
+    }
+    if (!pub_b && __any_sync(0xFFFFFFFFu, wb != 0)) {
+      if (leader) atomicAdd(&synd[1], 1);
+      pub_b = true;
+    }
+    const volatile int* vs = synd;
+    if ((!need_a || vs[0] != 0) && (!need_b || vs[1] != 0)) return;
+    parity_rows_early<BG, LANES, ABS, E, STEP>(p, zl, ZL, Lg, wa, wb, need_a, need_b, pub_a, pub_b, synd);
   }
 }
 
@@ -1004,9 +1029,33 @@ __device__ __forceinline__ void parity_rows(const KParams& p, uint32_t zl, uint3
 template <int BG, int MAXW, int LANES, bool ABS>
 __device__ __forceinline__ void local_check(const KParams& p, uint32_t zl, uint32_t ZL,
                                             const uint8_t* __restrict__ Lg, int* wcnt, int* mabs,
-                                            bool early = false, bool need_a = true, bool need_b = true) {
+                                            bool early = false, bool need_a = true, bool need_b = true,
+                                            int* synd = nullptr) {
   int wa = 0, wb = 0;
   bool stopped = false;
+  if constexpr (BG != 0) {
+    // full graph, early mode, group counters given: cooperative straight-line scan
+    if (early && synd && p.rows == RowW<BG>::n) {
+      const bool nb = LANES == 2 && need_b;
+      bool pub_a = !need_a, pub_b = !nb;
+      parity_rows_early<BG, LANES, ABS, 0, 4>(p, zl, ZL, Lg, wa, wb, need_a, nb, pub_a, pub_b, synd);
+      wcnt[0] = wcnt[1] = 0;  // already counted in synd
+      mabs[0] = mabs[1] = 255;  // only failing lanes stop early; the margin pass below is skipped
+      const volatile int* vs = synd;
+      if ((need_a && vs[0] == 0) || (nb && vs[1] == 0)) {
+        // a live lane may have a zero syndrome: its margin is needed
+        int ma[2] = {255, 255}, mb[2] = {255, 255};
+        for (int c = 0; c < p.n_blocks; ++c) {
+          const uint32_t u = ld_elem<LANES>(Lg + (uint32_t)c * ZL + zl);
+          ma[c & 1] = min(ma[c & 1], abs((int)(u & 0xFFu) - 128));
+          mb[c & 1] = min(mb[c & 1], abs((int)((u >> 8) & 0xFFu) - 128));
+        }
+        mabs[0] = min(ma[0], ma[1]);
+        mabs[1] = min(mb[0], mb[1]);
+      }
+      return;
+    }
+  }
   if constexpr (BG == 0) {
     for (int r = 0; r < p.rows; ++r) {
       const int e0 = p.row_start[r];
@@ -1315,7 +1364,7 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
                            lane_valid[1] && !gs.done[1], gs.synd);
       else
         local_check<BG, MAXW, LANES, ABS>(p, zl, ZL, Lg, wc, ma, early, lane_valid[0] && !gs.done[0],
-                                          lane_valid[1] && !gs.done[1]);
+                                          lane_valid[1] && !gs.done[1], gs.synd);
       if (active) {
 #pragma unroll
         for (int l = 0; l < LANES; ++l) {
@@ -1606,7 +1655,7 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const 
     {
       int wc[2], ma[2];
       if constexpr (TM) local_check_tm<BG>(p, zl, ZL, p.abs_base, wc, ma, !last[0] && !last[1], act[0], act[1], gs.synd);
-      else local_check<BG, MAXW, LANES, ABS>(p, zl, ZL, Lg, wc, ma, !last[0] && !last[1], act[0], act[1]);
+      else local_check<BG, MAXW, LANES, ABS>(p, zl, ZL, Lg, wc, ma, !last[0] && !last[1], act[0], act[1], gs.synd);
 #pragma unroll
       for (int l = 0; l < 2; ++l) {
         if (wc[l]) atomicAdd(&gs.synd[l], wc[l]);
