@@ -169,13 +169,39 @@ __device__ __forceinline__ void flt_row_parity(const KParams& p, uint32_t tq, co
   }
 }
 
-// The full syndrome of a full compile-time graph as straight-line code.
-template <int PREC, int BG, int R = 0>
+// The full syndrome of a full compile-time graph (rows R..E-1) as
+// straight-line code.
+template <int PREC, int BG, int R = 0, int E = RowW<BG>::n>
 __device__ __forceinline__ void flt_parity_rows(const KParams& p, const uint8_t* Lg, uint32_t zl, uint32_t ZL,
                                                 int (&wc)[2]) {
-  if constexpr (R < RowW<BG>::n) {
+  if constexpr (R < E) {
     flt_row_parity<PREC, RowW<BG>::w[R]>(p, row_tq<BG, R>(), Lg, zl, ZL, wc);
-    flt_parity_rows<PREC, BG, R + 1>(p, Lg, zl, ZL, wc);
+    flt_parity_rows<PREC, BG, R + 1, E>(p, Lg, zl, ZL, wc);
+  }
+}
+
+// Early-stop iterations (see local_check_tm): blocks of STEP straight-line
+// rows; a warp publishes a failing check of a live lane in the group's
+// counters at once, and all warps stop when every live lane has one.
+template <int PREC, int BG, int R, int STEP>
+__device__ __forceinline__ void flt_parity_rows_early(const KParams& p, const uint8_t* Lg, uint32_t zl, uint32_t ZL,
+                                                      int (&wc)[2], bool need_a, bool need_b, bool& pub_a,
+                                                      bool& pub_b, int* synd) {
+  if constexpr (R < RowW<BG>::n) {
+    constexpr int E = R + STEP < RowW<BG>::n ? R + STEP : RowW<BG>::n;
+    flt_parity_rows<PREC, BG, R, E>(p, Lg, zl, ZL, wc);
+    const bool leader = (threadIdx.x & 31) == 0;
+    if (!pub_a && __any_sync(0xFFFFFFFFu, wc[0] != 0)) {
+      if (leader) atomicAdd(&synd[0], 1);
+      pub_a = true;
+    }
+    if (!pub_b && __any_sync(0xFFFFFFFFu, wc[1] != 0)) {
+      if (leader) atomicAdd(&synd[1], 1);
+      pub_b = true;
+    }
+    const volatile int* vs = synd;
+    if ((!need_a || vs[0] != 0) && (!need_b || vs[1] != 0)) return;
+    flt_parity_rows_early<PREC, BG, E, STEP>(p, Lg, zl, ZL, wc, need_a, need_b, pub_a, pub_b, synd);
   }
 }
 
@@ -348,13 +374,24 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
     const bool last = it == p.max_iter;
     if (!(p.early_stop != NRLDPC_STOP_NONE || p.trace || last)) continue;
 
-    // end-of-iteration check (decoder.py:497-536)
+    // end-of-iteration check (decoder.py:497-536); early-stop iterations of
+    // full graphs cooperate (whole warps per group when Z % 32 == 0)
+    const bool early = BG != 0 && !p.trace && !last && p.z % 32 == 0 && p.early_stop != NRLDPC_STOP_NONE;
     if (active) {
       int wc[2] = {0, 0};
-      bool straight = false;
+      bool straight = false, coop = false;
+      const bool need_a = lane_valid[0] && !gs.done[0];
+      const bool need_b = LANES == 2 && lane_valid[1] && !gs.done[1];
       if constexpr (BG != 0) {
         if (p.rows == RowW<BG>::n) {
-          flt_parity_rows<PREC, BG>(p, Lg, zl, ZL, wc);
+          if (early) {
+            bool pub_a = !need_a, pub_b = !need_b;
+            flt_parity_rows_early<PREC, BG, 0, 4>(p, Lg, zl, ZL, wc, need_a, need_b, pub_a, pub_b, gs.synd);
+            wc[0] = wc[1] = 0;  // already counted in gs.synd
+            coop = true;
+          } else {
+            flt_parity_rows<PREC, BG>(p, Lg, zl, ZL, wc);
+          }
           straight = true;
         }
       }
@@ -374,7 +411,10 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
         }
       }
       float ma[2] = {__int_as_float(0x7F800000), __int_as_float(0x7F800000)};
-      for (int c = 0; c < p.n_blocks; ++c) {
+      // the margin matters only for a lane whose syndrome is zero
+      const volatile int* vs = gs.synd;
+      const bool margin = !coop || (need_a && vs[0] == 0) || (need_b && vs[1] == 0);
+      for (int c = 0; c < p.n_blocks && margin; ++c) {
         const uint32_t v = *reinterpret_cast<const uint32_t*>(Lg + (uint32_t)c * ZL + zl);
 #pragma unroll
         for (int l = 0; l < LANES; ++l) ma[l] = fminf(ma[l], F::lane_abs(v, l));
