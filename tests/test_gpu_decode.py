@@ -546,6 +546,7 @@ def test_tm_layout_matches_byte_pair_layout_and_oracle(cuda_ok, bg_id, z, rows, 
     (half2 posteriors, messages in shared and tensor memory; the lane-refill
     kernel too for early stops with batch > 2); NRLDPC_NO_TM=1 selects the
     byte-pair layout. Both must give the oracle's results."""
+    monkeypatch.delenv("NRLDPC_NO_TM", raising=False)  # the first plan must take the TM layout
     bg = nr.load_basegraph(bg_id, z)
     params = nr.code_params(bg, z, rows)
     if stop == "crc":
@@ -622,6 +623,7 @@ def test_float_on_chip_messages_match_workspace_and_oracle(cuda_ok, prec, bg_id,
     """Single-group BG1/BG2 float shapes keep their messages on chip (shared
     and tensor memory; BG1 core rows in the workspace); NRLDPC_NO_TM=1 keeps
     them all in the global workspace. Both must give the oracle's results."""
+    monkeypatch.delenv("NRLDPC_NO_TM", raising=False)  # the first plan must keep messages on chip
     bg = nr.load_basegraph(bg_id, z)
     params = nr.code_params(bg, z, rows)
     _, llr = noisy_llrs(bg, rows, 1.5, batch, seed=(z, rows, 5))
