@@ -13,9 +13,16 @@ exceeds the 126 MB L2, so no step reads a cached input.
 the same metric/config; it is the reference arm (the reference itself is
 pure numpy and publishes no GPU path).
 
-Under torchrun each rank drives its own GPU with its own shard (independent
-codewords, no collective on the data path: weak scaling); the step time is
-the max over ranks.
+Multi-GPU (north_star subsystem 5): ``--gpus N`` without torchrun drives N
+devices from one process (per-device plans, streams and pinned buffers, no
+process group, no NCCL). Under torchrun each rank drives its own GPU; a gloo
+group carries only the barrier and the max over ranks. Either way every GPU
+decodes its own shard of independent codewords (weak scaling) and the step
+time is the max over devices.
+
+The same line carries BASELINE configs 1, 3, 4 and 5 (``configs``, from
+tools/bench_configs.py), each with its roofline fraction and an oracle
+parity check of a sample in its CPU-baseline leg.
 """
 
 from __future__ import annotations
@@ -49,6 +56,8 @@ def parse():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip BASELINE configs 1/3/4/5")
+    ap.add_argument("--no-api", action="store_true", help="skip the decode(numpy) e2e_api leg")
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--chunks", type=int, default=12, help="e2e pipelining sub-batches")
     ap.add_argument("--overlap", type=int, default=2,
@@ -74,8 +83,8 @@ class ClockSampler:
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
-        self.index = index
+    def __init__(self, index):
+        self.index = ",".join(str(i) for i in index) if isinstance(index, (list, tuple)) else str(index)
         self.proc = None
         self.rows = []
 
@@ -137,9 +146,16 @@ def cpu_baseline(bg, rows, iters, threads: int, blocks: np.ndarray, k: int, gpu_
     t0 = time.perf_counter()
     ref = oracle.decode(sample, bg, cfg, threads=threads)
     dt = time.perf_counter() - t0
+    # one core, for the per-core figure BASELINE.md's CPU plan asks for
+    n1 = min(n, 16)
+    t1 = time.perf_counter()
+    oracle.decode(sample[:n1], bg, cfg, threads=1)
+    dt1 = time.perf_counter() - t1
     line = {"value": n * k / dt / 1e9, "unit": "Gbps", "cores": threads, "kind": "port",
             "sample": f"{n} codewords of the same workload (BG1 Z=384, 10 iterations), "
-                      f"oracle/ldpc_oracle.c over {threads} OpenMP threads, {dt:.2f} s wall"}
+                      f"oracle/ldpc_oracle.c over {threads} OpenMP threads, {dt:.2f} s wall",
+            "one_core": {"value": n1 * k / dt1 / 1e9, "unit": "Gbps", "cores": 1,
+                         "sample": f"{n1} codewords, 1 thread, {dt1:.2f} s wall"}}
     if gpu_out is not None:
         bits = nr.unpack_bits(gpu_out["bits"][:n], k)
         same = (np.array_equal(bits, ref["bits"])
@@ -202,77 +218,149 @@ def run_reference(args):
     return 0
 
 
+class DeviceArm:
+    """One GPU's share of the headline workload: its plan, rotating input
+    buffers (more than L2 holds), output buffers and streams."""
+
+    def __init__(self, device: int, seed_rank: int, args, bg, rows):
+        import torch
+        import paper_2009_05534_b200 as nr
+        from paper_2009_05534_b200.synth import noisy_llrs
+
+        self.device = device
+        self.dev = torch.device("cuda", device)
+        torch.cuda.set_device(self.dev)
+        self.params = nr.code_params(bg, bg.z, rows)
+        self.B = args.batch
+        self.cfg = nr.DecodeConfig(max_iter=args.iters, early_stop="none")
+        self.plan = nr.get_plan(bg, rows, self.cfg, device=device)
+        # synthetic AWGN traffic for this device's shard, quantized on the GPU
+        self.msgs, llr = noisy_llrs(bg, rows, 2.0, self.B, seed=(2024, seed_rank))
+        self.llr_dev = torch.from_numpy(llr).to(self.dev)
+        self.blocks0 = nr.quantize(self.llr_dev, nr.QuantConfig(), self.params)
+        per = self.blocks0.numel()
+        self.nbuf = max(2, int(np.ceil(2.0 * 126e6 / per)) + 1)
+        self.per = per
+        self.bufs = [torch.roll(self.blocks0, shifts=i, dims=0).contiguous() for i in range(self.nbuf)]
+        self.n_ov = max(1, args.overlap)
+        self.outs = [self.plan.alloc_outputs(self.B) for _ in range(max(2, self.n_ov))]
+        self.stream = torch.cuda.current_stream(self.dev)
+        self.side = [torch.cuda.Stream(device=self.dev) for _ in range(self.n_ov)]
+
+    def launch(self, i: int):
+        j = i % self.n_ov
+        self.plan.decode_device(self.bufs[i % self.nbuf], self.outs[j], stream=self.side[j].cuda_stream)
+
+    def begin(self):
+        import torch
+        self.t0 = torch.cuda.Event(enable_timing=True)
+        self.t1 = torch.cuda.Event(enable_timing=True)
+        self.t0.record(self.stream)
+        for s in self.side:
+            s.wait_stream(self.stream)
+
+    def end(self):
+        for s in self.side:
+            self.stream.wait_stream(s)
+        self.t1.record(self.stream)
+
+
+def pcie_bandwidth(device: int, nbytes: int):
+    """Measured pinned H2D / D2H copy rate (GB/s, best of 10) for one batch's
+    worth of bytes on ``device``."""
+    import torch
+    from paper_2009_05534_b200.hostmem import pinned_empty
+    h = pinned_empty((nbytes,), torch.uint8, device)
+    d = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{device}")
+    st = torch.cuda.Stream(device=device)
+    res = {}
+    for name, fn in (("h2d", lambda: d.copy_(h, non_blocking=True)), ("d2h", lambda: h.copy_(d, non_blocking=True))):
+        best = 1e9
+        with torch.cuda.stream(st):
+            for rep in range(12):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(st)
+                fn()
+                b.record(st)
+                b.synchronize()
+                if rep >= 2:
+                    best = min(best, a.elapsed_time(b))
+        res[name] = nbytes / (best * 1e-3) / 1e9
+    return res
+
+
 def run_ours(args):
     import torch
-    import torch.distributed as dist
+    import paper_2009_05534_b200 as nr
+    from paper_2009_05534_b200 import _native
+    from paper_2009_05534_b200.hostmem import numa_note, pinned_empty
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2009_05534_b200.shard import resolve_devices, run_per_device
+    dist = None
+    # torchrun: one process per GPU; the gloo group only carries the barrier
+    # and the max over ranks (CPU tensors), the decode never communicates.
+    # Otherwise one process drives N devices: per-device plans, buffers and
+    # streams, no process group and no NCCL (north_star subsystem 5).
+    try:
+        devices = resolve_devices(args.gpus, torch.cuda.device_count(), world, local)
+    except ValueError as e:
+        raise SystemExit(str(e))
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-    torch.cuda.set_device(dev)
-
-    import paper_2009_05534_b200 as nr
-    from paper_2009_05534_b200 import _native
-    from paper_2009_05534_b200.synth import noisy_llrs
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    n_gpus = world if world > 1 else len(devices)
 
     bg, rows, edges = workload()
     params = nr.code_params(bg, bg.z, rows)
     B = args.batch
     k = params.k
-    cfg = nr.DecodeConfig(max_iter=args.iters, early_stop="none")
-    plan = nr.get_plan(bg, rows, cfg, device=local)
+    arms = [DeviceArm(d, rank * len(devices) + i, args, bg, rows) for i, d in enumerate(devices)]
+    a0 = arms[0]
+    dev0 = a0.dev
+    torch.cuda.set_device(dev0)
 
-    # synthetic AWGN traffic for this rank's shard, quantized on the GPU
-    msgs, llr = noisy_llrs(bg, rows, 2.0, B, seed=(2024, rank))
-    llr_dev = torch.from_numpy(llr).to(dev)
-    blocks0 = nr.quantize(llr_dev, nr.QuantConfig(), params)
     # the quantize kernel (north_star subsystem 1) on its own: float64 LLRs
     # in, int8 blocks out; HBM-bound
     q_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     for _ in range(3):
-        nr.quantize(llr_dev, nr.QuantConfig(), params)
-    torch.cuda.synchronize(dev)
+        nr.quantize(a0.llr_dev, nr.QuantConfig(), params)
+    torch.cuda.synchronize(dev0)
     q_ev[0].record()
     for _ in range(20):
-        nr.quantize(llr_dev, nr.QuantConfig(), params)
+        nr.quantize(a0.llr_dev, nr.QuantConfig(), params)
     q_ev[1].record()
-    torch.cuda.synchronize(dev)
+    torch.cuda.synchronize(dev0)
     quant_ms = q_ev[0].elapsed_time(q_ev[1]) / 20
     quant_bytes = B * (8 * params.n_tx + params.n_c)
-    del llr, llr_dev
-    # rotate inputs so the set of live inputs exceeds L2 (126 MB)
-    per = blocks0.numel()
-    nbuf = max(2, int(np.ceil(2.0 * 126e6 / per)) + 1)
-    bufs = [torch.roll(blocks0, shifts=i, dims=0).contiguous() for i in range(nbuf)]
-    n_ov = max(1, args.overlap)
-    outs = [plan.alloc_outputs(B) for _ in range(max(2, n_ov))]
-    stream = torch.cuda.current_stream(dev)
-    side = [torch.cuda.Stream(device=dev) for _ in range(n_ov)]
+    for a in arms:
+        del a.llr_dev
 
-    for i in range(args.warmup):
-        plan.decode_device(bufs[i % nbuf], outs[i % 2])
-    torch.cuda.synchronize(dev)
+    for a in arms:
+        for i in range(args.warmup):
+            a.plan.decode_device(a.bufs[i % a.nbuf], a.outs[i % 2])
+    for a in arms:
+        torch.cuda.synchronize(a.dev)
 
     # correctness / BLER of one decode (outside the timed region)
-    plan.decode_device(bufs[0], outs[0])
-    torch.cuda.synchronize(dev)
-    gpu_host = {key: outs[0][key].cpu().numpy() for key in ("bits", "iters", "synd", "success")}
+    plan = a0.plan
+    plan.decode_device(a0.bufs[0], a0.outs[0])
+    torch.cuda.synchronize(dev0)
+    gpu_host = {key: a0.outs[0][key].cpu().numpy() for key in ("bits", "iters", "synd", "success")}
     bits = nr.unpack_bits(gpu_host["bits"], k)
-    bler = float((bits != msgs).any(axis=1).mean())
-    success = float(outs[0]["success"].float().mean().item())
+    bler = float((bits != a0.msgs).any(axis=1).mean())
+    success = float(a0.outs[0]["success"].float().mean().item())
     # the same inputs with the reference's syndrome early stop (quality check;
     # fixed-iteration int8 decoding overshoots in the reference itself)
     cfg_s = nr.DecodeConfig(max_iter=args.iters, early_stop="syndrome")
-    plan_s = nr.get_plan(bg, rows, cfg_s, device=local)
+    plan_s = nr.get_plan(bg, rows, cfg_s, device=devices[0])
     out_s = plan_s.alloc_outputs(B)
-    plan_s.decode_device(bufs[0], out_s)
-    torch.cuda.synchronize(dev)
+    plan_s.decode_device(a0.bufs[0], out_s)
+    torch.cuda.synchronize(dev0)
     bits_s = nr.unpack_bits(out_s["bits"].cpu().numpy(), k)
-    quality = {"bler_syndrome_stop": float((bits_s != msgs).any(axis=1).mean()),
+    quality = {"bler_syndrome_stop": float((bits_s != a0.msgs).any(axis=1).mean()),
                "mean_iterations_syndrome_stop": float(out_s["iters"].float().mean().item()),
                "note": "bler/success_rate are for the benchmarked fixed-iteration mode and match the "
                        "reference bit for bit: its int8 engine with early_stop='none' diverges once "
@@ -280,51 +368,51 @@ def run_ours(args):
                        "cfg2_bg1_z384_none10 records success=0 for the reference itself)"}
 
     # (1) batch latency and per-launch kernel time: one stream, back to back
-    n_lat = min(args.steps, 100)
+    n_lat = min(max(args.steps, 20), 100)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(n_lat)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(n_lat)]
-    torch.cuda.synchronize(dev)
+    torch.cuda.synchronize(dev0)
     for i in range(n_lat):
-        starts[i].record(stream)
-        plan.decode_device(bufs[i % nbuf], outs[i % 2])
-        ends[i].record(stream)
-    torch.cuda.synchronize(dev)
+        starts[i].record(a0.stream)
+        plan.decode_device(a0.bufs[i % a0.nbuf], a0.outs[i % 2])
+        ends[i].record(a0.stream)
+    torch.cuda.synchronize(dev0)
     step_ms = np.array([s.elapsed_time(e) for s, e in zip(starts, ends)])
 
-    # (2) throughput: K consecutive independent batches, alternating over
-    # n_ov streams, bracketed by events on the launching stream
-    t_all0 = torch.cuda.Event(enable_timing=True)
-    t_all1 = torch.cuda.Event(enable_timing=True)
-    if world > 1:
+    # (2) throughput: K consecutive independent batches per device,
+    # alternating over n_ov streams, bracketed by events on each device's
+    # launching stream; time = max over devices (and ranks)
+    if dist is not None:
         dist.barrier()
-    torch.cuda.synchronize(dev)
-    sampler = ClockSampler(local)
+    for a in arms:
+        torch.cuda.synchronize(a.dev)
+    sampler = ClockSampler(devices)
     with sampler:
-        t_all0.record(stream)
-        for s in side:
-            s.wait_stream(stream)
+        for a in arms:
+            a.begin()
         for i in range(args.steps):
-            j = i % n_ov
-            plan.decode_device(bufs[i % nbuf], outs[j], stream=side[j].cuda_stream)
-        for s in side:
-            stream.wait_stream(s)
-        t_all1.record(stream)
-        torch.cuda.synchronize(dev)
-    launches = args.steps  # one decode kernel per step
-    total_ms = t_all0.elapsed_time(t_all1)
-    if world > 1:
-        t = torch.tensor([total_ms], device=dev)
+            for a in arms:
+                a.launch(i)
+        for a in arms:
+            a.end()
+        for a in arms:
+            torch.cuda.synchronize(a.dev)
+    launches = args.steps * len(arms)  # one decode kernel per step per device
+    per_dev_ms = [a.t0.elapsed_time(a.t1) for a in arms]
+    total_ms = max(per_dev_ms)
+    if dist is not None:
+        t = torch.tensor([total_ms])
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
         dist.barrier()
     ms_per_step = total_ms / args.steps
-    value = B * world * k * args.steps / (total_ms * 1e-3) / 1e9
+    value = B * n_gpus * k * args.steps / (total_ms * 1e-3) / 1e9
 
     # roofline: ALU (half2) pipe, algorithmic ops per launch / kernel time
     import ctypes
-    a, m = ctypes.c_double(), ctypes.c_double()
-    _native.check(_native.load().nrldpc_alu_peak(local, ctypes.byref(a), ctypes.byref(m)))
-    lane_peak = m.value  # lane-ops/s, dual-pipe issue ceiling
+    am, mm = ctypes.c_double(), ctypes.c_double()
+    _native.check(_native.load().nrldpc_alu_peak(devices[0], ctypes.byref(am), ctypes.byref(mm)))
+    lane_peak = mm.value  # lane-ops/s, dual-pipe issue ceiling
     rho = 2  # codeword values per 32-bit lane in the half2 kernels
     peak_ops = lane_peak * rho
     kern_ms = float(step_ms.mean())
@@ -334,9 +422,9 @@ def run_ours(args):
     # DRAM bytes per launch of this kernel from the committed ncu --set full
     # capture (profiles/); ncu does not run inside the bench
     traffic, traffic_note = None, "no committed ncu capture"
-    tfile = ROOT / "profiles" / "r01_ncu_decode_traffic.json"
-    if tfile.is_file():
-        tj = json.loads(tfile.read_text())
+    tfiles = sorted((ROOT / "profiles").glob("r*_ncu_decode_traffic.json"))
+    if tfiles:
+        tj = json.loads(tfiles[-1].read_text())
         traffic = tj["traffic_bytes_per_launch"]
         traffic_note = (f"bytes/launch, dram__bytes_read.sum + dram__bytes_write.sum of {tj['kernel']} "
                         f"({tj['source']}); the algorithmic input alone is {B * params.n_c} bytes")
@@ -345,20 +433,23 @@ def run_ours(args):
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
 
     line = {
-        "metric": METRIC, "value": value, "unit": "Gbps", "n_gpus": world,
+        "metric": METRIC, "value": value, "unit": "Gbps", "n_gpus": n_gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
         "data": "synthetic: random messages, systematic encode, BPSK, AWGN Eb/N0 2.0 dB, "
                 "L=2y/sigma^2, GPU quantize (scale 8)",
         "config": {"workload": WORKLOAD, "graph": "BG1", "z": 384, "rows_used": rows,
-                   "codewords_per_gpu": B, "global_batch": B * world, "iterations": args.iters,
+                   "codewords_per_gpu": B, "global_batch": B * n_gpus, "iterations": args.iters,
                    "early_stop": "none", "beta": 0.75, "lanes": plan.lanes,
                    "codewords_per_cta": plan.codewords_per_cta, "threads_per_cta": plan.threads_per_cta,
                    "smem_bytes": plan.smem_bytes,
-                   "l2": f"inputs rotate over {nbuf} buffers ({nbuf * per / 1e6:.0f} MB > 126 MB L2)",
-                   "parallelism": f"batch shard x{world}, no collective",
-                   "overlap": f"{n_ov} streams: consecutive independent batches alternate, so one "
+                   "l2": f"inputs rotate over {a0.nbuf} buffers ({a0.nbuf * a0.per / 1e6:.0f} MB > 126 MB L2)",
+                   "parallelism": (f"{n_gpus} processes (torchrun), gloo barrier/max only" if dist is not None
+                                   else f"one process driving {n_gpus} device(s)") +
+                                  ": batch shard per GPU, no collective, no NCCL",
+                   "overlap": f"{a0.n_ov} streams per device: consecutive independent batches alternate, so one "
                               f"batch's partial last wave shares the SMs with the next batch's first"},
+        "per_device_ms": per_dev_ms,
         "p50_batch_latency_ms": float(np.median(step_ms)),
         "p99_batch_latency_ms": float(np.percentile(step_ms, 99)),
         "bler": bler, "success_rate": success, "quality": quality,
@@ -367,9 +458,10 @@ def run_ours(args):
             "frac": achieved / peak_ops, "traffic": traffic,
             "traffic_note": traffic_note,
             "note": f"{OPS_PER_EDGE} algorithmic int ops per edge-update per codeword (SURVEY 8d) x "
-                    f"{edges} edges x Z x iterations x B per launch / mean kernel time; peak = measured "
-                    f"half2 dual-pipe lane-op rate {lane_peak / 1e12:.2f} T/s (ALU pipe alone "
-                    f"{a.value / 1e12:.2f} T/s, nrldpc_alu_peak) x {rho} codewords per lane",
+                    f"{edges} edges x Z x iterations x B per launch / mean kernel time (one stream, "
+                    f"back to back); peak = measured half2 dual-pipe lane-op rate {lane_peak / 1e12:.2f} T/s "
+                    f"(ALU pipe alone {am.value / 1e12:.2f} T/s, nrldpc_alu_peak) x {rho} codewords per lane",
+            "frac_overlapped": alg_ops * args.steps * len(arms) / (total_ms * 1e-3) / (peak_ops * len(arms)),
         },
         "roofline_quantize": {"bound": "hbm", "achieved": quant_bytes / (quant_ms * 1e-3) / 1e9,
                               "peak": hbm_peak, "unit": "GB/s",
@@ -385,81 +477,156 @@ def run_ours(args):
         "clocks": sampler.summary(),
     }
 
-    # end-to-end through the C-ABI host entry points (pinned host buffers):
-    # every step copies its int8 inputs in and its results out inside the
-    # timed region. Pipelined: step i+1 is enqueued before waiting for step i
-    # (nrldpc_decode_host_async + nrldpc_host_wait, two calls in flight), the
-    # way a serving loop feeds consecutive batches. The synchronous call
-    # (nrldpc_decode_host, one batch at a time) is reported beside it.
+    # end-to-end through the C-ABI host entry points (pinned host buffers on
+    # the GPU's NUMA node): every step copies its int8 inputs in and its
+    # results out inside the timed region. Pipelined: step i+1 is enqueued
+    # before waiting for step i (nrldpc_decode_host_async + nrldpc_host_wait,
+    # two calls in flight), the way a serving loop feeds consecutive batches.
+    # One host thread per device (ctypes releases the GIL); time = the slowest
+    # device. The synchronous call (nrldpc_decode_host) is reported beside it.
     if not args.no_e2e:
-        import torch as _t
-        hin, hout = [], []
-        for j in range(2):
-            host_in = _t.empty((B, params.n_c), dtype=_t.int8, pin_memory=True)
-            host_in.copy_(bufs[j].cpu())
-            hin.append(host_in.numpy())
-            hout.append(plan.host_outputs(B, pinned=True))
+        pcie = pcie_bandwidth(devices[0], B * params.n_c)
+        d2h = B * (4 * plan.words + 4 + 4 + 1 + 1)
         chunks = args.chunks
-        for _ in range(max(1, args.warmup)):
-            plan.decode_host(hin[0], chunks=chunks, out=hout[0])
-        # warm both pipeline slots (their device buffers are allocated on first use)
-        warm = [plan.decode_host_async(hin[j], chunks=chunks, out=hout[j])[0] for j in range(2)]
-        for w in warm:
-            plan.host_wait(w)
+        host = []
+        for a in arms:
+            hin, hout = [], []
+            for j in range(2):
+                t_in = pinned_empty((B, params.n_c), torch.int8, a.device)
+                t_in.copy_(a.bufs[j].cpu())
+                hin.append(t_in.numpy())
+                hout.append(a.plan.host_outputs(B, pinned=True))
+            host.append((hin, hout))
+            for _ in range(max(1, args.warmup)):
+                a.plan.decode_host(hin[0], chunks=chunks, out=hout[0])
+            # warm both pipeline slots (their device buffers are allocated on first use)
+            warm = [a.plan.decode_host_async(hin[j], chunks=chunks, out=hout[j])[0] for j in range(2)]
+            for w in warm:
+                a.plan.host_wait(w)
 
-        def timed(fn):
-            if world > 1:
+        def run_threads(fn):
+            if dist is not None:
                 dist.barrier()
-            t0 = time.perf_counter()
-            launches_ = fn()
-            dt_ = time.perf_counter() - t0
-            if world > 1:
-                tt = torch.tensor([dt_], device=dev)
+            dt_, ns = run_per_device(len(arms), fn, setup=lambda ix: torch.cuda.set_device(arms[ix].dev))
+            if dist is not None:
+                tt = torch.tensor([dt_])
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
                 dt_ = float(tt.item())
-            return dt_, launches_
+            return dt_, sum(ns)
 
-        def run_sync():
+        def run_sync(ix):
             n = 0
+            pl, (hin, hout) = arms[ix].plan, host[ix]
             for i in range(args.steps):
-                plan.decode_host(hin[i % 2], chunks=chunks, out=hout[i % 2])
+                pl.decode_host(hin[i % 2], chunks=chunks, out=hout[i % 2])
                 n += _native.launch_count()
             return n
 
-        def run_pipelined():
+        def run_pipelined(ix):
             n, prev = 0, None
+            pl, (hin, hout) = arms[ix].plan, host[ix]
             for i in range(args.steps):
-                ticket, _ = plan.decode_host_async(hin[i % 2], chunks=chunks, out=hout[i % 2])
+                ticket, _ = pl.decode_host_async(hin[i % 2], chunks=chunks, out=hout[i % 2])
                 n += _native.launch_count()
                 if prev is not None:
-                    plan.host_wait(prev)
+                    pl.host_wait(prev)
                 prev = ticket
-            plan.host_wait(prev)
+            pl.host_wait(prev)
             return n
 
-        dt_sync, _ = timed(run_sync)
-        ref_bits = [hout[j]["bits"].copy() for j in range(2)]
-        dt, e2e_launch = timed(run_pipelined)
-        same = all(np.array_equal(hout[j]["bits"], ref_bits[j]) for j in range(2))
-        d2h = B * (4 * plan.words + 4 + 4 + 1 + 1)
-        line["e2e"] = {"value": B * world * k * args.steps / dt / 1e9, "unit": "Gbps",
-                       "h2d_bytes_per_step": B * params.n_c, "d2h_bytes_per_step": d2h,
+        dt_sync, _ = run_threads(run_sync)
+        ref_bits = [[h[1][j]["bits"].copy() for j in range(2)] for h in host]
+        dt, e2e_launch = run_threads(run_pipelined)
+        same = all(np.array_equal(h[1][j]["bits"], ref_bits[ix][j]) for ix, h in enumerate(host) for j in range(2))
+        e2e_val = B * n_gpus * k * args.steps / dt / 1e9
+        h2d_bound = k / (params.n_c / (pcie["h2d"] * 1e9)) / 1e9 * n_gpus  # Gbps if only the input copy mattered
+        line["e2e"] = {"value": e2e_val, "unit": "Gbps",
+                       "h2d_bytes_per_step": B * params.n_c * n_gpus, "d2h_bytes_per_step": d2h * n_gpus,
                        "ms_per_step": dt / args.steps * 1e3, "chunks": chunks,
                        "gpu_launches": e2e_launch,
-                       "path": "nrldpc_decode_host_async + nrldpc_host_wait (C ABI), two batches in flight: "
-                               "pinned H2D, decode, D2H per step",
-                       "sync_value": B * world * k * args.steps / dt_sync / 1e9,
+                       "path": "nrldpc_decode_host_async + nrldpc_host_wait (C ABI), two batches in flight "
+                               "per device: pinned H2D, decode, D2H per step",
+                       "pinned": numa_note(devices[0]),
+                       "pcie_measured_gbs": pcie,
+                       "h2d_bound_gbps": h2d_bound,
+                       "frac_of_bound": e2e_val / min(value, h2d_bound),
+                       "bound_note": "bound = min(device-resident value, info rate the measured pinned H2D "
+                                     "copy rate allows)",
+                       "sync_value": B * n_gpus * k * args.steps / dt_sync / 1e9,
                        "sync_path": "nrldpc_decode_host (C ABI), one batch per call",
                        "pipelined_matches_sync": bool(same)}
+        if rank == 0 and not args.no_api:
+            line["e2e_api"] = e2e_api(bg, a0, args, k)
 
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and not args.no_configs:
+        sys.path.insert(0, str(ROOT / "tools"))
+        import bench_configs
+        torch.cuda.set_device(dev0)
+        cfg_lines, cfg_samples = bench_configs.run_all(peak_ops, devices=devices)
+        line["configs"] = cfg_lines
+    if rank == 0 and not args.no_cpu:
         threads = host_threads(args.cpu_threads)
-        line["cpu_baseline"] = cpu_baseline(bg, rows, args.iters, threads, blocks0.cpu().numpy(), k, gpu_host)
+        if n_gpus == 1:
+            line["cpu_baseline"] = cpu_baseline(bg, rows, args.iters, threads, a0.blocks0.cpu().numpy(), k,
+                                                gpu_host)
+        if not args.no_configs:
+            for cl, smp in zip(line["configs"], cfg_samples):
+                cl["cpu_baseline"] = cpu_parity(smp, threads)
+                cl["parity"] = cl["cpu_baseline"]["parity"]["bit_exact"]
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist is not None:
         dist.destroy_process_group()
     return 0
+
+
+def e2e_api(bg, a0, args, k):
+    """The reference-facing call (decoder.py:543): ``decode(numpy int8 (B,
+    n_c), bg, cfg)`` -> DecodeResult with (B, K) bit bytes, from an ordinary
+    (pageable) numpy array, as the reference's harness and CLI call it after
+    integrate.install_into_ldpclab()."""
+    import paper_2009_05534_b200 as nr
+    arrs = [np.ascontiguousarray(a0.bufs[j].cpu().numpy()) for j in range(2)]
+    cfg = a0.cfg
+    for j in range(3):
+        nr.decode(arrs[j % 2], bg, cfg)
+    steps = max(5, min(args.steps, 50))
+    t0 = time.perf_counter()
+    for i in range(steps):
+        res = nr.decode(arrs[i % 2], bg, cfg)
+    dt = time.perf_counter() - t0
+    B = arrs[0].shape[0]
+    return {"value": B * k * steps / dt / 1e9, "unit": "Gbps", "ms_per_step": dt / steps * 1e3,
+            "steps": steps, "h2d_bytes_per_step": int(arrs[0].nbytes), "d2h_bytes_per_step": int(B * (4 * a0.plan.words + 10)),
+            "result_bytes_per_step": int(res.bits.nbytes),
+            "path": "paper_2009_05534_b200.decode(numpy pageable int8, bg, cfg) -> DecodeResult (bits unpacked "
+                    "to (B, K) bytes); the drop-in the reference's callers reach",
+            "device": a0.device}
+
+
+def cpu_parity(samples, threads):
+    """CPU-baseline leg of one config: the oracle port decodes the config's
+    sample codewords on the host cores (timed), and its outputs are the
+    bit-exact parity check of the GPU's results for the same codewords."""
+    from oracle import oracle
+    import paper_2009_05534_b200 as nr
+    n_cw, k_total, same, t = 0, 0, True, 0.0
+    for bg, cfg, blocks, gpu in samples:
+        t0 = time.perf_counter()
+        ref = oracle.decode(blocks, bg, cfg, threads=threads)
+        t += time.perf_counter() - t0
+        k = bg.k_b * bg.z
+        bits = nr.unpack_bits(gpu["bits"], k)
+        same = same and (np.array_equal(bits, ref["bits"])
+                         and np.array_equal(gpu["iters"], ref["iterations"])
+                         and np.array_equal(gpu["synd"], ref["syndrome_weight"])
+                         and np.array_equal(gpu["success"].astype(bool), ref["success"]))
+        n_cw += len(blocks)
+        k_total += len(blocks) * k
+    return {"value": k_total / t / 1e9, "unit": "Gbps", "cores": threads, "kind": "port",
+            "sample": f"{n_cw} codewords of the config ({len(samples)} shape group(s)), oracle/ldpc_oracle.c",
+            "parity": {"codewords": n_cw, "bit_exact": bool(same),
+                       "vs": "oracle (pinned to the reference's golden vectors)"}}
 
 
 def main():

@@ -133,18 +133,21 @@ int nrldpc_decode(nrldpc_plan* plan, const void* llr, int64_t batch,
 /*
  * Flooding-schedule decode (decoder.py:337-365, 569-581): every row reads the
  * previous iteration's posteriors, then L = sat(L_b + sum of messages).
- * Same buffers and early-stop semantics as nrldpc_decode (device pointers).
+ * Same buffers, status word and early-stop semantics as nrldpc_decode
+ * (device pointers).
  */
 int nrldpc_decode_flooding(nrldpc_plan* plan, const void* llr, int64_t batch, uint32_t* bits,
                            int32_t* iters, int32_t* synd, uint8_t* success, uint8_t* crc_ok,
-                           int32_t* trace_w, float* trace_m, void* stream);
+                           int32_t* trace_w, float* trace_m, int32_t* status, void* stream);
 
 /*
  * Host-buffer entry point (the end-to-end path): llr_host (batch, n_c) and
- * outputs are HOST pointers. The library stages through pinned buffers and
- * pipelines H2D copy / decode / D2H copy over `chunks` sub-batches on its
- * own streams, then synchronizes. Returns NRLDPC_EINVAL if an int8 input
- * exceeded |127|.
+ * outputs are HOST pointers. It pipelines H2D copy / decode / D2H copy over
+ * `chunks` sub-batches on the plan's own streams, then synchronizes. Pinned
+ * buffers are used in place; pageable ones are staged through the plan's
+ * pinned buffers (inputs copied in by the library's host threads, chunk by
+ * chunk, overlapped with the DMA; results copied out when the call
+ * retires). Returns NRLDPC_EINVAL if an int8 input exceeded |127|.
  */
 int nrldpc_decode_host(nrldpc_plan* plan, const void* llr_host, int64_t batch,
                        uint32_t* bits, int32_t* iters, int32_t* synd,
@@ -192,6 +195,14 @@ int nrldpc_alu_peak(int device, double* alu_lane_ops_per_s, double* mixed_lane_o
  * every m in [0,127] (the kernel then skips its lookup table). Host only.
  */
 int nrldpc_beta_rule(double beta, int* mode, float* beta_h, float* delta, float* c);
+
+/*
+ * Host helper for the reference's result layout (decoder.py:332-334):
+ * packed hard decisions (batch, words_per_cw) uint32, LSB-first, -> (batch,
+ * k) bytes 0/1. Multi-threaded on the library's host pool. Host pointers.
+ */
+int nrldpc_unpack_bits(const uint32_t* words, int64_t batch, int64_t words_per_cw, int64_t k,
+                       uint8_t* out);
 
 /* Number of kernel launches the last nrldpc_decode/_quantize issued. */
 int nrldpc_launch_count(void);

@@ -38,6 +38,7 @@ EXPORTS = (
     "nrldpc_decode_flooding",
     "nrldpc_encode",
     "nrldpc_channel_awgn",
+    "nrldpc_unpack_bits",
     "nrldpc_launch_count",
     "nrldpc_alu_peak",
     "nrldpc_beta_rule",
@@ -90,7 +91,7 @@ def load() -> ctypes.CDLL:
     lib.nrldpc_decode_host_async.restype = c_int
     lib.nrldpc_host_wait.argtypes = [c_void_p, c_int64]
     lib.nrldpc_host_wait.restype = c_int
-    lib.nrldpc_decode_flooding.argtypes = [c_void_p, c_void_p, c_int64] + [c_void_p] * 8
+    lib.nrldpc_decode_flooding.argtypes = [c_void_p, c_void_p, c_int64] + [c_void_p] * 9
     lib.nrldpc_decode_flooding.restype = c_int
     lib.nrldpc_encode.argtypes = [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]
     lib.nrldpc_encode.restype = c_int
@@ -101,6 +102,8 @@ def load() -> ctypes.CDLL:
     lib.nrldpc_alu_peak.restype = c_int
     lib.nrldpc_beta_rule.argtypes = [c_double, c_void_p, c_void_p, c_void_p, c_void_p]
     lib.nrldpc_beta_rule.restype = c_int
+    lib.nrldpc_unpack_bits.argtypes = [c_void_p, c_int64, c_int64, c_int64, c_void_p]
+    lib.nrldpc_unpack_bits.restype = c_int
     lib.nrldpc_launch_count.argtypes = []
     lib.nrldpc_launch_count.restype = c_int
     lib.nrldpc_last_error.argtypes = []

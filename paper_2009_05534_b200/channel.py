@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -65,7 +66,7 @@ def ebn0_to_sigma(ebn0_db: float, rate_eff: float) -> float:
     return math.sqrt(1.0 / (2.0 * rate_eff * ebn0))
 
 
-_QPLANS: dict = {}
+_QPLANS: "OrderedDict" = OrderedDict()
 
 
 def _quant_plan(params):
@@ -76,10 +77,15 @@ def _quant_plan(params):
     plan = _QPLANS.get(key)
     if plan is None:
         from .basegraph import load_basegraph
-        from .decoder import DecodeConfig, get_plan
+        from .decoder import PLAN_CACHE_MAX, DecodeConfig, get_plan
         k_b = params.n_c // params.z - params.rows_used
         bg = load_basegraph(1 if k_b == 22 else 2, params.z)
         plan = _QPLANS[key] = get_plan(bg, params.rows_used, DecodeConfig(), device=key[3])
+        # bounded like the decoder's plan cache (least recently used out)
+        while len(_QPLANS) > max(1, PLAN_CACHE_MAX):
+            _QPLANS.popitem(last=False)
+    else:
+        _QPLANS.move_to_end(key)
     return plan
 
 

@@ -14,8 +14,12 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
+#include <condition_variable>
+#include <functional>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <bitset>
 #include <vector>
 
@@ -1938,6 +1942,7 @@ struct Shape {
   int threads = 0;  // 0: no feasible shape
   size_t smem = 0;
   int occ = 0;      // resident CTAs per SM (0: not queried yet)
+  int refill_occ = 0;  // the same for this shape's lane-refill kernel
   bool abs = false; // kp.cb holds absolute shared-window addresses
   bool tm = false;  // TM layout (half2 L, shared/tensor-memory messages)
   KParams kp{};
@@ -1975,8 +1980,28 @@ struct nrldpc_plan {
     int32_t* h_status = nullptr;  // pinned: the slot's status word lands here
     cudaEvent_t done = nullptr;   // recorded after the slot's result copies
     int64_t ticket = -1;          // call in flight in this slot (-1: none)
+    // pageable callers: inputs are staged through h_in (parallel host copy
+    // into pinned memory, chunk by chunk, overlapped with the chunks' DMA);
+    // results land in h_out and are copied to the caller's buffers when the
+    // call retires
+    uint8_t* h_in = nullptr;
+    size_t h_in_cap = 0;
+    uint8_t* h_out = nullptr;
+    size_t h_out_cap = 0;
+    struct Dst {
+      void* p;
+      size_t off, n;
+    } dst[5] = {};
+    int n_dst = 0;
   } slot[kSlots];
   int64_t next_ticket = 0;
+  // Calls retired on behalf of a later call (slot reuse, or a synchronous
+  // call draining the pipeline) whose input was rejected: their status is
+  // kept here until their own nrldpc_host_wait, so an error is reported
+  // against the call that caused it and never fails the call reusing the
+  // slot. Bounded: the oldest entries go first.
+  std::vector<int64_t> failed;
+  static constexpr size_t kMaxFailed = 4096;
 };
 
 namespace {
@@ -2417,6 +2442,7 @@ Shape tm_shape(const nrldpc_plan* p, const Shape& leg) {
   Shape sh = leg;
   sh.tm = true;
   sh.occ = 0;
+  sh.refill_occ = 0;
   sh.smem = std::max(smem_for(1, lb, mb), one_per_sm);
   sh.kp.l_bytes = (uint32_t)lb;
   sh.kp.m_bytes = (uint32_t)mb;
@@ -2442,16 +2468,23 @@ template <int BG, int MAXW, int NREG, bool TM = false>
 static cudaError_t launch_refill(Shape& sh, int device, const int8_t* llr, long long batch, const KOut& o,
                                  cudaStream_t st) {
   static bool attr_done[64] = {};
-  static int occ_cache[64] = {}, sms[64] = {};
+  static int sms[64] = {};
   auto kern = k_decode_i8_refill<BG, MAXW, NREG, TM>;
   const int d = device & 63;
   if (!attr_done[d]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cache[d], kern, sh.threads, sh.smem);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms[d], cudaDevAttrMultiProcessorCount, device);
     if (e != cudaSuccess) return e;
-    if (occ_cache[d] < 1) occ_cache[d] = 1;
     attr_done[d] = true;
+  }
+  // occupancy depends on this shape's threads and shared memory (one
+  // instantiation serves several Z / rows_used): cached in the Shape, set at
+  // plan creation (the llr == nullptr call)
+  if (!sh.refill_occ) {
+    int occ = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, sh.threads, sh.smem);
+    if (e != cudaSuccess) return e;
+    sh.refill_occ = occ > 0 ? occ : 1;
   }
   if (!llr) return cudaSuccess;
   KParams kp = sh.kp;
@@ -2459,7 +2492,7 @@ static cudaError_t launch_refill(Shape& sh, int device, const int8_t* llr, long 
   kp.trace = 0;
   kp.vec_load = ((long long)kp.n_blocks * kp.z) % 16 == 0 && ((uintptr_t)llr & 15) == 0;
   const long long pairs = (batch + 1) / 2;
-  const long long grid = std::min<long long>(pairs, (long long)occ_cache[d] * sms[d]);
+  const long long grid = std::min<long long>(pairs, (long long)sh.refill_occ * sms[d]);
   int32_t* work = nullptr;
   cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&work), sizeof(int32_t), device, st);
   if (e != cudaSuccess) return e;
@@ -2567,6 +2600,126 @@ static cudaError_t launch_float(int schedule, Shape& sh, int device, const void*
   return launch_float_bg<PREC, 0>(sh, device, llr, batch, o, st);
 }
 
+// ---- host worker pool -------------------------------------------------------
+// A few persistent threads for the host side of the end-to-end path: copying
+// a pageable caller's input into pinned staging memory, and unpacking packed
+// hard decisions into the reference's (B, K) byte layout. One copy thread
+// moves ~10 GB/s; the pool splits each chunk so the host copy keeps ahead
+// of the PCIe DMA it feeds. NRLDPC_HOST_THREADS overrides the size.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool pool;
+    return pool;
+  }
+  int size() const { return (int)workers_.size() + 1; }
+  // f(i) for i in [0, n): the caller runs tasks too; returns when all done
+  void run(int n, const std::function<void(int)>& f) {
+    if (n <= 0) return;
+    if (n == 1 || workers_.empty()) {
+      for (int i = 0; i < n; ++i) f(i);
+      return;
+    }
+    std::unique_lock<std::mutex> call(call_mu_);  // one parallel job at a time
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = &f;
+      n_ = n;
+      next_.store(0);
+      left_.store(n);
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return left_.load() == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    int n = (int)std::thread::hardware_concurrency();
+    if (const char* e = std::getenv("NRLDPC_HOST_THREADS")) n = std::atoi(e);
+    n = std::max(1, std::min(n, 8));
+    for (int i = 0; i + 1 < n; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  void work() {
+    for (;;) {
+      const int i = next_.fetch_add(1);
+      if (i >= n_) return;
+      (*job_)(i);
+      if (left_.fetch_sub(1) == 1) {
+        std::lock_guard<std::mutex> lk(mu_);
+        done_cv_.notify_all();
+      }
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        if (!job_) continue;
+      }
+      work();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_, call_mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* job_ = nullptr;
+  int n_ = 0;
+  std::atomic<int> next_{0}, left_{0};
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+static void host_copy(void* dst, const void* src, size_t n) {
+  constexpr size_t kPiece = 1u << 20;
+  HostPool& pool = HostPool::get();
+  const int parts = (int)std::min<size_t>((size_t)pool.size(), (n + kPiece - 1) / kPiece);
+  if (parts <= 1) {
+    std::memcpy(dst, src, n);
+    return;
+  }
+  const size_t per = ((n + parts - 1) / parts + 4095) & ~size_t(4095);
+  pool.run(parts, [&](int i) {
+    const size_t o = (size_t)i * per;
+    if (o < n) std::memcpy(static_cast<uint8_t*>(dst) + o, static_cast<const uint8_t*>(src) + o, std::min(per, n - o));
+  });
+}
+
+static bool is_pageable(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+static cudaError_t grow_pinned(uint8_t*& buf, size_t& cap, size_t need) {
+  if (need <= cap) return cudaSuccess;
+  if (buf) cudaFreeHost(buf);
+  buf = nullptr;
+  cap = 0;
+  const cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&buf), need);
+  if (e == cudaSuccess) cap = need;
+  return e;
+}
+
 extern "C" {
 
 const char* nrldpc_last_error(void) { return g_last_error.c_str(); }
@@ -2592,7 +2745,7 @@ int nrldpc_beta_rule(double beta, int* mode, float* beta_h, float* delta, float*
 
 int nrldpc_decode_flooding(nrldpc_plan* plan, const void* llr, int64_t batch, uint32_t* bits,
                            int32_t* iters, int32_t* synd, uint8_t* success, uint8_t* crc_ok,
-                           int32_t* trace_w, float* trace_m, void* stream) {
+                           int32_t* trace_w, float* trace_m, int32_t* status, void* stream) {
   g_launches = 0;
   if (!plan) return fail(NRLDPC_EINVAL, "plan is NULL");
   if (batch < 0) return fail(NRLDPC_EINVAL, "batch must be non-negative");
@@ -2621,7 +2774,7 @@ int nrldpc_decode_flooding(nrldpc_plan* plan, const void* llr, int64_t batch, ui
   const int threads = (plan->z + 31) / 32 * 32;
   void* ws = nullptr;
   NR_CUDA(scratch_alloc(&ws, (size_t)batch * plan->n_edges * plan->z * 4, plan->device, st));
-  KOut o{bits, iters, synd, success, crc_ok, trace_w, trace_m, nullptr};
+  KOut o{bits, iters, synd, success, crc_ok, trace_w, trace_m, status};
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -2711,6 +2864,36 @@ int nrldpc_alu_peak(int device, double* alu_lane_ops_per_s, double* mixed_lane_o
 }
 
 int nrldpc_launch_count(void) { return g_launches; }
+
+int nrldpc_unpack_bits(const uint32_t* words, int64_t batch, int64_t words_per_cw, int64_t k, uint8_t* out) {
+  if (batch < 0 || k < 0 || words_per_cw * 32 < k) return fail(NRLDPC_EINVAL, "bad unpack shape");
+  if (batch == 0 || k == 0) return NRLDPC_OK;
+  if (!words || !out) return fail(NRLDPC_EINVAL, "NULL buffer");
+  // byte b of a packed word -> 8 output bytes 0/1, LSB first
+  static const auto lut = [] {
+    std::vector<uint64_t> t(256);
+    for (int b = 0; b < 256; ++b) {
+      uint64_t v = 0;
+      for (int i = 0; i < 8; ++i) v |= (uint64_t)((b >> i) & 1) << (8 * i);
+      t[b] = v;
+    }
+    return t;
+  }();
+  HostPool& pool = HostPool::get();
+  const int64_t per = std::max<int64_t>(1, (batch + 4 * pool.size() - 1) / (4 * pool.size()));
+  const int parts = (int)((batch + per - 1) / per);
+  pool.run(parts, [&](int part) {
+    const int64_t c0 = part * per, c1 = std::min(batch, c0 + per);
+    for (int64_t c = c0; c < c1; ++c) {
+      const uint8_t* src = reinterpret_cast<const uint8_t*>(words + c * words_per_cw);
+      uint8_t* dst = out + c * k;
+      const int64_t full = k / 8;
+      for (int64_t i = 0; i < full; ++i) std::memcpy(dst + 8 * i, &lut[src[i]], 8);
+      for (int64_t i = full * 8; i < k; ++i) dst[i] = (src[i >> 3] >> (i & 7)) & 1u;
+    }
+  });
+  return NRLDPC_OK;
+}
 
 int nrldpc_plan_create(int device, int k_b, int z, int rows_used, const int32_t* row_start,
                        const int16_t* cols, const int16_t* shifts, int precision, double beta,
@@ -2994,6 +3177,8 @@ int nrldpc_plan_destroy(nrldpc_plan* plan) {
     if (sl.done) cudaEventSynchronize(sl.done), cudaEventDestroy(sl.done);
     if (sl.d_buf) cudaFree(sl.d_buf);
     if (sl.h_status) cudaFreeHost(sl.h_status);
+    if (sl.h_in) cudaFreeHost(sl.h_in);
+    if (sl.h_out) cudaFreeHost(sl.h_out);
   }
   if (plan->d_crc_tab) cudaFree(plan->d_crc_tab);
   cudaSetDevice(prev);
@@ -3162,11 +3347,20 @@ static int host_enqueue(nrldpc_plan* plan, int si, const void* llr_host, int64_t
     plan->chunk_ev.push_back(e);
   }
   int launches = 0;
+  // a pageable input is staged through pinned memory chunk by chunk: the
+  // host copy of chunk i+1 overlaps the DMA of chunk i (a pageable source
+  // would make every cudaMemcpyAsync a synchronous, driver-staged copy)
+  const bool stage_in = is_pageable(llr_host);
+  if (stage_in) NR_CUDA(grow_pinned(sl.h_in, sl.h_in_cap, batch * per_cw_in));
   for (int idx = 0; idx < n_chunks; ++idx) {
     const int64_t b0 = idx * chunk;
     const int64_t nb = std::min<int64_t>(chunk, batch - b0);
-    NR_CUDA(cudaMemcpyAsync(d_llr + b0 * per_cw_in, static_cast<const uint8_t*>(llr_host) + b0 * per_cw_in,
-                            nb * per_cw_in, cudaMemcpyHostToDevice, cin));
+    const uint8_t* src = static_cast<const uint8_t*>(llr_host) + b0 * per_cw_in;
+    if (stage_in) {
+      host_copy(sl.h_in + b0 * per_cw_in, src, nb * per_cw_in);
+      src = sl.h_in + b0 * per_cw_in;
+    }
+    NR_CUDA(cudaMemcpyAsync(d_llr + b0 * per_cw_in, src, nb * per_cw_in, cudaMemcpyHostToDevice, cin));
     NR_CUDA(cudaEventRecord(plan->chunk_ev[idx], cin));
     cudaStream_t st = plan->streams[2 + idx % n_comp];
     NR_CUDA(cudaStreamWaitEvent(st, plan->chunk_ev[idx], 0));
@@ -3181,11 +3375,37 @@ static int host_enqueue(nrldpc_plan* plan, int si, const void* llr_host, int64_t
     NR_CUDA(cudaEventRecord(plan->chunk_ev[n_chunks + c], plan->streams[2 + c]));
     NR_CUDA(cudaStreamWaitEvent(cout, plan->chunk_ev[n_chunks + c], 0));
   }
-  NR_CUDA(cudaMemcpyAsync(bits, d_bits, batch * words * 4, cudaMemcpyDeviceToHost, cout));
-  NR_CUDA(cudaMemcpyAsync(iters, d_iters, batch * 4, cudaMemcpyDeviceToHost, cout));
-  NR_CUDA(cudaMemcpyAsync(synd, d_synd, batch * 4, cudaMemcpyDeviceToHost, cout));
-  NR_CUDA(cudaMemcpyAsync(success, d_succ, batch, cudaMemcpyDeviceToHost, cout));
-  if (crc_ok) NR_CUDA(cudaMemcpyAsync(crc_ok, d_crc, batch, cudaMemcpyDeviceToHost, cout));
+  // results: straight into pinned caller buffers; pageable ones get the
+  // slot's pinned staging area and a host copy when the call retires (a D2H
+  // copy into pageable memory would block this enqueue until it completes)
+  struct Out {
+    void* host;
+    const void* dev;
+    size_t n;
+  } outs[5] = {{bits, d_bits, (size_t)batch * words * 4}, {iters, d_iters, (size_t)batch * 4},
+               {synd, d_synd, (size_t)batch * 4}, {success, d_succ, (size_t)batch},
+               {crc_ok, d_crc, crc_ok ? (size_t)batch : 0}};
+  sl.n_dst = 0;
+  size_t stage_bytes = 0;
+  bool staged[5] = {};
+  for (int i = 0; i < 5; ++i) {
+    if (outs[i].n && is_pageable(outs[i].host)) {
+      staged[i] = true;
+      stage_bytes += align16(outs[i].n);
+    }
+  }
+  if (stage_bytes) NR_CUDA(grow_pinned(sl.h_out, sl.h_out_cap, stage_bytes));
+  size_t so = 0;
+  for (int i = 0; i < 5; ++i) {
+    if (!outs[i].n) continue;
+    void* dst = outs[i].host;
+    if (staged[i]) {
+      sl.dst[sl.n_dst++] = {outs[i].host, so, outs[i].n};
+      dst = sl.h_out + so;
+      so += align16(outs[i].n);
+    }
+    NR_CUDA(cudaMemcpyAsync(dst, outs[i].dev, outs[i].n, cudaMemcpyDeviceToHost, cout));
+  }
   NR_CUDA(cudaMemcpyAsync(sl.h_status, d_status, 4, cudaMemcpyDeviceToHost, cout));
   NR_CUDA(cudaEventRecord(sl.done, cout));
   *launches_out = launches;
@@ -3193,12 +3413,22 @@ static int host_enqueue(nrldpc_plan* plan, int si, const void* llr_host, int64_t
 }
 
 // Retire the call in slot `si`: wait for its results and report its status.
-static int host_retire(nrldpc_plan* plan, int si) {
+// own == false: the retire happens on behalf of another call (the slot is
+// being reused, or a synchronous call drains the pipeline); a rejected input
+// is then recorded against the retired call's ticket for its own wait
+// instead of failing the caller.
+static int host_retire(nrldpc_plan* plan, int si, bool own) {
   auto& sl = plan->slot[si];
   if (sl.ticket < 0) return NRLDPC_OK;
+  const int64_t t = sl.ticket;
   sl.ticket = -1;
   NR_CUDA(cudaEventSynchronize(sl.done));
-  if (*sl.h_status) return fail(NRLDPC_EINVAL, "int8 LLR magnitudes must be at most 127");
+  for (int i = 0; i < sl.n_dst; ++i) host_copy(sl.dst[i].p, sl.h_out + sl.dst[i].off, sl.dst[i].n);
+  sl.n_dst = 0;
+  if (!*sl.h_status) return NRLDPC_OK;
+  if (own) return fail(NRLDPC_EINVAL, "int8 LLR magnitudes must be at most 127");
+  if (plan->failed.size() >= nrldpc_plan::kMaxFailed) plan->failed.erase(plan->failed.begin());
+  plan->failed.push_back(t);
   return NRLDPC_OK;
 }
 
@@ -3222,7 +3452,7 @@ int nrldpc_decode_host(nrldpc_plan* plan, const void* llr_host, int64_t batch, u
   NR_CUDA(cudaSetDevice(plan->device));
   // a synchronous call retires whatever is still in flight first
   for (int i = 0; i < nrldpc_plan::kSlots; ++i) {
-    rc = host_retire(plan, i);
+    rc = host_retire(plan, i, false);
     if (rc != NRLDPC_OK) return rc;
   }
   static const bool dbg = getenv("NRLDPC_HOST_TIMING") != nullptr;
@@ -3237,7 +3467,7 @@ int nrldpc_decode_host(nrldpc_plan* plan, const void* llr_host, int64_t batch, u
   if (rc != NRLDPC_OK) return rc;
   plan->slot[0].ticket = plan->next_ticket++;
   if (dbg) cudaEventRecord(t1, plan->streams[1]);
-  rc = host_retire(plan, 0);
+  rc = host_retire(plan, 0, true);
   if (dbg) {
     float ms = 0;
     cudaEventSynchronize(t1);
@@ -3266,7 +3496,8 @@ int nrldpc_decode_host_async(nrldpc_plan* plan, const void* llr_host, int64_t ba
     return NRLDPC_OK;
   }
   const int si = (int)(t % nrldpc_plan::kSlots);
-  rc = host_retire(plan, si);  // the slot's previous call (its caller may still wait: already done)
+  // the slot's previous call; its status stays with its own ticket
+  rc = host_retire(plan, si, false);
   if (rc != NRLDPC_OK) return rc;
   int launches = 0;
   rc = host_enqueue(plan, si, llr_host, batch, bits, iters, synd, success, crc_ok, chunks, &launches);
@@ -3282,8 +3513,15 @@ int nrldpc_host_wait(nrldpc_plan* plan, int64_t ticket) {
   std::lock_guard<std::mutex> lock(plan->host_mu);
   NR_CUDA(cudaSetDevice(plan->device));
   for (int i = 0; i < nrldpc_plan::kSlots; ++i)
-    if (plan->slot[i].ticket == ticket) return host_retire(plan, i);
-  return NRLDPC_OK;  // already retired (or an empty batch)
+    if (plan->slot[i].ticket == ticket) return host_retire(plan, i, true);
+  // already retired on behalf of a later call: report its own status
+  for (auto it = plan->failed.begin(); it != plan->failed.end(); ++it) {
+    if (*it == ticket) {
+      plan->failed.erase(it);
+      return fail(NRLDPC_EINVAL, "int8 LLR magnitudes must be at most 127");
+    }
+  }
+  return NRLDPC_OK;  // retired ok (or an empty batch)
 }
 
 }  // extern "C"

@@ -102,11 +102,16 @@ __global__ void __launch_bounds__(384) k_decode_flood(const __grid_constant__ KP
   const bool on = z < Z;
   V* M = reinterpret_cast<V*>(ws) + cw * (long long)p.n_edges * Z;  // [edge][z]
 
+  bool bad = false;
   for (long long n = z; n < n_c; n += blockDim.x) {
     const V v = F::from_in(llr, cw * n_c + n);
+    // int8 inputs must satisfy |x| <= 127 (decoder.py:287-288): -128 is the
+    // only int8 value outside, and the host raises the reference's ValueError
+    if (PREC == NRLDPC_INT8) bad |= ((const int8_t*)llr)[cw * n_c + n] == -128;
     L[n] = v;
     Lb[n] = v;
   }
+  if (bad && o.status) atomicOr(o.status, 1);
   for (long long i = z; i < (long long)p.n_edges * Z; i += blockDim.x) M[i] = V(0);
   if (z == 0) {
     s_synd = 0;

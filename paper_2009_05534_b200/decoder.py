@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import ctypes
 import threading
+from collections import OrderedDict
 from dataclasses import dataclass
 from enum import Enum
 
@@ -174,6 +175,7 @@ class Plan:
             out["bits"].data_ptr(), out["iters"].data_ptr(), out["synd"].data_ptr(),
             out["success"].data_ptr(), out["crc_ok"].data_ptr(),
             tw.data_ptr() if tw is not None else None, tm.data_ptr() if tm is not None else None,
+            out["status"].data_ptr() if "status" in out else None,
             stream))
 
     def decode_device(self, llr, out: dict, stream=None) -> None:
@@ -202,11 +204,12 @@ class Plan:
         if not pinned:
             return {k: np.empty(s, d) for k, (s, d) in shapes.items()}
         import torch
+
+        from .hostmem import pinned_empty
         tdt = {np.uint32: torch.int32, np.int32: torch.int32, np.uint8: torch.uint8}
         out = {}
         for k, (s, d) in shapes.items():
-            t = torch.empty(s, dtype=tdt[d], pin_memory=True)
-            out[k] = t.numpy().view(d)
+            out[k] = pinned_empty(s, tdt[d], self.device).numpy().view(d)  # on the GPU's NUMA node
         return out
 
     def decode_host_async(self, llr: np.ndarray, chunks: int = 12, out: dict | None = None) -> tuple[int, dict]:
@@ -242,7 +245,12 @@ class Plan:
         return out
 
 
-_PLAN_CACHE: dict = {}
+# Plans cached per (graph, Z, rows_used, config, device), least recently used
+# first out. An evicted plan is destroyed (nrldpc_plan_destroy: its streams,
+# events and staging buffers) once nothing else holds it, so a long BLER sweep
+# over many shapes through the drop-in keeps a bounded footprint.
+PLAN_CACHE_MAX = 128
+_PLAN_CACHE: "OrderedDict" = OrderedDict()
 _PLAN_LOCK = threading.Lock()
 
 
@@ -255,6 +263,10 @@ def get_plan(bg, rows_used: int, cfg: DecodeConfig, device: int = 0, coscheduled
         if plan is None:
             plan = Plan(bg, rows_used, cfg, device, coscheduled)
             _PLAN_CACHE[key] = plan
+            while len(_PLAN_CACHE) > max(1, PLAN_CACHE_MAX):
+                _PLAN_CACHE.popitem(last=False)
+        else:
+            _PLAN_CACHE.move_to_end(key)
         return plan
 
 
@@ -272,10 +284,15 @@ def _graph_fingerprint(bg, rows_used: int) -> int:
 
 
 def unpack_bits(words: np.ndarray, k: int) -> np.ndarray:
-    """(B, ceil(K/32)) LSB-first uint32 words -> (B, K) uint8 0/1."""
-    w = np.ascontiguousarray(words).view(np.uint32).astype("<u4", copy=False)
-    bits = np.unpackbits(w.view(np.uint8).reshape(w.shape[0], -1), axis=1, bitorder="little")
-    return bits if bits.shape[1] == k else np.ascontiguousarray(bits[:, :k])
+    """(B, ceil(K/32)) LSB-first uint32 words -> (B, K) uint8 0/1
+    (decoder.py:332-334 layout), on the library's host threads."""
+    w = np.ascontiguousarray(words).view(np.uint32)
+    if w.ndim != 2 or w.shape[1] * 32 < k:
+        raise ValueError("unpack_bits needs (B, ceil(K/32)) words")
+    out = np.empty((w.shape[0], int(k)), np.uint8)
+    _native.check(_native.load().nrldpc_unpack_bits(w.ctypes.data, w.shape[0], w.shape[1], int(k),
+                                                    out.ctypes.data))
+    return out
 
 
 def _rows_used(n_c: int, bg) -> int:
@@ -325,6 +342,8 @@ def decode(llrs, bg, cfg: DecodeConfig, trace: list | None = None) -> DecodeResu
         batch = int(host.shape[0])
         if batch == 0:
             return _empty_result(plan.k, cfg)
+        # pageable arrays are staged through the plan's pinned buffers by the
+        # library's host threads, overlapped with the chunks' DMA
         out = plan.decode_host(host, chunks=max(1, min(12, batch // 86)))
         return DecodeResult(
             bits=unpack_bits(out["bits"], plan.k),
@@ -438,7 +457,12 @@ def decode_flooding(llrs, bg, cfg: DecodeConfig, trace: list | None = None) -> D
         x = torch.from_numpy(np.ascontiguousarray(arr)).to(f"cuda:{plan.device}")
     else:
         if cfg.precision is Precision.INT8:
-            x = x.to(torch.int8)
+            if x.dtype != torch.int8:
+                wide = x.to(torch.int32)
+                if wide.numel() and int(wide.abs().max()) > INT8_SAT:
+                    raise ValueError("int8 LLR magnitudes must be at most 127")
+                x = wide
+            x = x.to(torch.int8)  # an int8 -128 is flagged by the kernel (status word)
         else:
             x = x.to(torch.float16 if cfg.precision is Precision.F16 else torch.float32)
         plan = get_plan(bg, rows_used, cfg, device=x.device.index or 0)

@@ -16,7 +16,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .decoder import DecodeConfig, DecodeResult, get_plan, unpack_bits
+from .decoder import INT8_SAT, DecodeConfig, DecodeResult, get_plan, unpack_bits
 
 
 @dataclass
@@ -71,12 +71,19 @@ class MixedBatchDecoder:
     def _launch_all(self):
         import torch
         cur = torch.cuda.current_stream(self._device)
+        # the status words (int8 -128 seen) restart at zero on every replay
+        for out in self.outputs:
+            out["status"].zero_()
         for s in self._streams:
             s.wait_stream(cur)
         for i, si in self._order:
             self.plans[i].decode_device(self.inputs[i], self.outputs[i], stream=self._streams[si].cuda_stream)
         for s in self._streams:
             cur.wait_stream(s)
+
+    def describe(self) -> str:
+        return (f"one CUDA-graph replay: {len(self.plans)} per-shape launches over "
+                f"{len(self._streams)} streams (longest first)")
 
     def capture(self):
         import torch
@@ -95,12 +102,30 @@ class MixedBatchDecoder:
         self._graph.replay()
 
     def decode(self, llrs: list) -> list[DecodeResult]:
-        """Host arrays (or tensors) in, one DecodeResult per group out."""
+        """Host arrays (or tensors) in, one DecodeResult per group out.
+
+        Inputs are validated like ``decode`` (decoder.py:287-288): a wider
+        integer input outside [-127, 127] raises before anything runs, and an
+        int8 -128 is flagged by the kernels and raises after the replay."""
         import torch
+        if len(llrs) != len(self.inputs):
+            raise ValueError(f"expected {len(self.inputs)} groups, got {len(llrs)}")
+        int8 = self.cfg.precision.value == "int8"
         for x, src in zip(self.inputs, llrs):
-            x.copy_(src if isinstance(src, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(src)))
+            t = src if isinstance(src, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(src))
+            if tuple(t.shape) != tuple(x.shape):
+                raise ValueError(f"group input shape {tuple(t.shape)} != {tuple(x.shape)}")
+            if int8 and t.dtype != torch.int8:
+                wide = t.to(torch.int32)  # astype semantics, decoder.py:286
+                if wide.numel() and int(wide.abs().max()) > INT8_SAT:
+                    raise ValueError("int8 LLR magnitudes must be at most 127")
+                t = wide
+            x.copy_(t)
         self.replay()
         results = []
+        for plan, out in zip(self.plans, self.outputs):
+            if int(out["status"].item()):  # synchronizes with the replay
+                raise ValueError("int8 LLR magnitudes must be at most 127")
         for plan, out in zip(self.plans, self.outputs):
             h = {k: v.cpu().numpy() for k, v in out.items() if k in ("bits", "iters", "synd", "success", "crc_ok")}
             results.append(DecodeResult(

@@ -180,3 +180,60 @@ class MultiDeviceDecoder:
                               crc_ok=o["crc_ok"].astype(bool) if crc else None)
                  for o in outs if o["iters"].shape[0]]
         return merge_results(parts) if parts else _empty_result(self.k, self.cfg)
+
+
+def resolve_devices(gpus: int, visible: int, world: int = 1, local_rank: int = 0) -> list[int]:
+    """Devices one bench/serving process drives.
+
+    Under a launcher (world > 1) each process owns its LOCAL_RANK device.
+    Otherwise one process drives ``gpus`` devices itself (per-device plans
+    and streams, no process group). Asking for more devices than are visible
+    is an error, never a silent fallback to fewer."""
+    if world > 1:
+        if not 0 <= local_rank < max(visible, 1):
+            raise ValueError(f"LOCAL_RANK {local_rank} has no visible device ({visible} visible)")
+        return [int(local_rank)]
+    gpus = max(1, int(gpus))
+    if gpus > visible:
+        raise ValueError(f"--gpus {gpus} requested but only {visible} CUDA devices are visible")
+    return list(range(gpus))
+
+
+def run_per_device(n: int, fn, setup=None) -> tuple[float, list]:
+    """Run ``fn(i)`` for i < n on n host threads released together; returns
+    (wall seconds of the slowest, [results in device order]). ``setup(i)``
+    runs on the thread before the common start (e.g. set the CUDA device).
+    A worker's exception is re-raised."""
+    import threading
+    import time
+
+    res = [None] * n
+    err = []
+    bar = threading.Barrier(n + 1)
+
+    def work(i):
+        try:
+            if setup is not None:
+                setup(i)
+        except BaseException as e:  # noqa: BLE001
+            err.append(e)
+        bar.wait()
+        if err:
+            return
+        t0 = time.perf_counter()
+        try:
+            out = fn(i)
+        except BaseException as e:  # noqa: BLE001
+            err.append(e)
+            return
+        res[i] = (time.perf_counter() - t0, out)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(n)]
+    for t in th:
+        t.start()
+    bar.wait()
+    for t in th:
+        t.join()
+    if err:
+        raise err[0]
+    return max(r[0] for r in res), [r[1] for r in res]

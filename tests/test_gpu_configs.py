@@ -1,0 +1,166 @@
+"""GPU parity at the BASELINE configs' real sizes, and the error paths of the
+host/mixed/flooding entry points.
+
+* config 4: all 51 Z x {BG1, BG2} (102 groups x 16 codewords) in ONE mixed
+  batch, against the oracle group by group;
+* config 5: the slot-scale 7,488-codeword batch (BG1 rows_used=8, Z in
+  {384, 352, 320}) against the oracle;
+* errors are reported against the call that caused them (async host path),
+  and the mixed-batch / flooding device paths reject int8 -128 like
+  decode() does (decoder.py:287-288).
+"""
+
+import gc
+import weakref
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2009_05534_b200 as nr
+from paper_2009_05534_b200.synth import noisy_llrs
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _same(res, ref):
+    bad = np.flatnonzero((res.bits != ref["bits"]).any(axis=1))
+    assert bad.size == 0, f"bits differ in codewords {bad[:10]}"
+    assert np.array_equal(res.iterations, ref["iterations"])
+    assert np.array_equal(res.success, ref["success"])
+    assert np.array_equal(res.syndrome_weight, ref["syndrome_weight"])
+
+
+@pytest.mark.parametrize("stop", ["none", "syndrome"])
+def test_config4_full_mixed_batch_vs_oracle(cuda_ok, stop):
+    """BASELINE config 4 at full size: 102 groups of 16 codewords, one mixed
+    batch (MixedBatchDecoder), every group bit-exact against the oracle."""
+    from paper_2009_05534_b200.mixed import Group, MixedBatchDecoder
+    cfg = nr.DecodeConfig(max_iter=10, early_stop=stop)
+    groups, data = [], []
+    for bg_id in ("BG1", "BG2"):
+        for z in nr.ALL_LIFTING_SIZES:
+            bg = nr.load_basegraph(bg_id, z)
+            _, llr = noisy_llrs(bg, bg.m_bg, 2.0, 16, seed=(int(bg_id[-1]), z))
+            groups.append(Group(bg, bg.m_bg, 16))
+            data.append(oracle.quantize_i8(llr, z))
+    assert len(groups) == 102
+    mixed = MixedBatchDecoder(groups, cfg, streams=32)
+    for rep in range(2):  # capture, then a replay
+        results = mixed.decode(data)
+        for g, res, blocks in zip(groups, results, data):
+            _same(res, oracle.decode(blocks, g.bg, cfg))
+
+
+def test_config5_slot_batch_vs_oracle(cuda_ok):
+    """BASELINE config 5: 7,488 codewords (64 cell-slots x 117), BG1
+    rows_used=8, Z in {384, 352, 320}, 10 fixed iterations."""
+    cfg = nr.DecodeConfig(max_iter=10, early_stop="none")
+    per = 7488 // 3
+    for z in (384, 352, 320):
+        bg = nr.load_basegraph("BG1", z)
+        _, llr = noisy_llrs(bg, 8, 3.0, per, seed=(5, z))
+        blocks = oracle.quantize_i8(llr, z)
+        plan = nr.get_plan(bg, 8, cfg)
+        out = plan.alloc_outputs(per)
+        plan.decode_device(torch.from_numpy(blocks).cuda(), out)
+        torch.cuda.synchronize()
+        ref = oracle.decode(blocks, bg, cfg)
+        assert np.array_equal(nr.unpack_bits(out["bits"].cpu().numpy(), plan.k), ref["bits"]), z
+        assert np.array_equal(out["iters"].cpu().numpy(), ref["iterations"])
+        assert np.array_equal(out["synd"].cpu().numpy(), ref["syndrome_weight"])
+
+
+def _blocks(bg, n, seed, ebn0=1.5):
+    _, llr = noisy_llrs(bg, bg.m_bg, ebn0, n, seed=seed)
+    return oracle.quantize_i8(llr, bg.z)
+
+
+def test_async_error_stays_with_its_own_ticket(cuda_ok):
+    """bad, ok, ok issued without waiting: the third call retires the bad
+    call's slot on its behalf. The bad call must fail at its own wait, the
+    other two must succeed with correct results."""
+    bg = nr.load_basegraph("BG2", 128)
+    cfg = nr.DecodeConfig(max_iter=6)
+    plan = nr.Plan(bg, bg.m_bg, cfg)
+    good = [_blocks(bg, 7, (i, 3)) for i in range(3)]
+    refs = [oracle.decode(b, bg, cfg) for b in good]
+    bad = good[0].copy()
+    bad[3, 11] = -128
+    ins = [torch.from_numpy(x).pin_memory().numpy() for x in (bad, good[1], good[2])]
+    outs = [plan.host_outputs(7, pinned=True) for _ in range(3)]
+    t = [plan.decode_host_async(ins[i], chunks=2, out=outs[i])[0] for i in range(3)]
+    plan.host_wait(t[1])
+    plan.host_wait(t[2])
+    with pytest.raises(ValueError, match="at most 127"):
+        plan.host_wait(t[0])
+    plan.host_wait(t[0])  # reported once
+    for i in (1, 2):
+        assert np.array_equal(nr.unpack_bits(outs[i]["bits"], plan.k), refs[i]["bits"])
+        assert np.array_equal(outs[i]["iters"], refs[i]["iterations"])
+    # a synchronous call draining a bad call in flight succeeds; the bad call
+    # still fails at its own wait
+    tb, _ = plan.decode_host_async(ins[0], chunks=2, out=outs[0])
+    res = plan.decode_host(good[2], chunks=2)
+    assert np.array_equal(nr.unpack_bits(res["bits"], plan.k), refs[2]["bits"])
+    with pytest.raises(ValueError, match="at most 127"):
+        plan.host_wait(tb)
+
+
+def test_mixed_batch_rejects_out_of_range_inputs(cuda_ok):
+    from paper_2009_05534_b200.mixed import Group, MixedBatchDecoder
+    cfg = nr.DecodeConfig(max_iter=4)
+    shapes = [("BG1", 64), ("BG2", 384)]
+    groups, data = [], []
+    for bg_id, z in shapes:
+        bg = nr.load_basegraph(bg_id, z)
+        groups.append(Group(bg, bg.m_bg, 5))
+        data.append(_blocks(bg, 5, (z, 1)))
+    mixed = MixedBatchDecoder(groups, cfg, streams=2)
+    ok = mixed.decode(data)
+    bad = [d.copy() for d in data]
+    bad[1][2, 7] = -128
+    with pytest.raises(ValueError, match="at most 127"):
+        mixed.decode(bad)
+    wide = [d.astype(np.int32) for d in data]
+    wide[0][0, 0] = 200
+    with pytest.raises(ValueError, match="at most 127"):
+        mixed.decode(wide)
+    again = mixed.decode([d.astype(np.int32) for d in data])  # status reset per replay
+    for a, b in zip(ok, again):
+        assert np.array_equal(a.bits, b.bits) and np.array_equal(a.iterations, b.iterations)
+
+
+def test_flooding_device_path_rejects_out_of_range(cuda_ok):
+    bg = nr.load_basegraph("BG2", 16)
+    blocks = _blocks(bg, 4, (16, 2))
+    cfg = nr.DecodeConfig(max_iter=5)
+    ref = nr.decode_flooding(blocks, bg, cfg)
+    x = torch.from_numpy(blocks).cuda()
+    got = nr.decode_flooding(x, bg, cfg)
+    assert np.array_equal(got.bits, ref.bits)
+    bad = x.clone()
+    bad[1, 40] = -128
+    with pytest.raises(ValueError, match="at most 127"):
+        nr.decode_flooding(bad, bg, cfg)
+    wide = x.to(torch.int32)
+    wide[0, 3] = 300
+    with pytest.raises(ValueError, match="at most 127"):
+        nr.decode_flooding(wide, bg, cfg)
+
+
+def test_plan_cache_is_bounded_and_releases_plans(cuda_ok, monkeypatch):
+    from paper_2009_05534_b200 import decoder
+    monkeypatch.setattr(decoder, "PLAN_CACHE_MAX", 3)
+    cfg = nr.DecodeConfig(max_iter=3, beta=0.625)  # keys nothing else uses
+    refs = []
+    for z in (8, 10, 12, 14, 16, 18):
+        bg = nr.load_basegraph("BG2", z)
+        refs.append(weakref.ref(decoder.get_plan(bg, bg.m_bg, cfg)))
+        assert len(decoder._PLAN_CACHE) <= 3
+    gc.collect()
+    assert sum(r() is None for r in refs) >= 3  # evicted plans were destroyed
+    bg = nr.load_basegraph("BG2", 18)
+    res = nr.decode(_blocks(bg, 2, (18, 0)), bg, cfg)  # the cache still works
+    assert res.bits.shape == (2, 10 * 18)

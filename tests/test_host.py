@@ -218,3 +218,22 @@ def test_install_into_reference_package_rebinds_and_restores():
         assert ldpclab.decoder.decode is orig
     finally:
         sys.path.remove(str(ref))
+
+
+@pytest.mark.parametrize("batch,k", [(0, 64), (1, 70), (7, 8448), (33, 3840), (5, 2)])
+def test_native_unpack_bits_matches_numpy(batch, k):
+    """nrldpc_unpack_bits (host threads, byte LUT) == numpy unpackbits LSB-first."""
+    from paper_2009_05534_b200.decoder import unpack_bits
+    words = (k + 31) // 32
+    rng = np.random.default_rng(batch * 1000 + k)
+    w = rng.integers(0, 2**32, size=(batch, words), dtype=np.uint64).astype(np.uint32)
+    ref = np.unpackbits(w.view(np.uint8).reshape(batch, 4 * words), axis=1, bitorder="little")[:, :k]
+    assert np.array_equal(unpack_bits(w, k), ref)
+
+
+def test_hostmem_cpulist_parser(tmp_path, monkeypatch):
+    from paper_2009_05534_b200 import hostmem
+    assert hostmem.node_cpus(10**6) == set()          # absent node: empty set, no error
+    assert hostmem.gpu_numa_node(0) is None or hostmem.gpu_numa_node(0) >= 0
+    with hostmem.on_gpu_node(0):                        # no GPU here: a no-op
+        pass

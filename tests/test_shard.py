@@ -153,3 +153,45 @@ def test_multi_device_decoder_shards_and_merges_in_order(batch, devices):
     assert np.array_equal(res.bits, ref["bits"])
     assert np.array_equal(res.iterations, ref["iterations"])
     assert np.array_equal(res.syndrome_weight, ref["syndrome_weight"])
+
+
+def test_resolve_devices_never_falls_back_silently():
+    from paper_2009_05534_b200.shard import resolve_devices
+    assert resolve_devices(4, 8) == [0, 1, 2, 3]
+    assert resolve_devices(1, 1) == [0]
+    assert resolve_devices(8, 8, world=8, local_rank=5) == [5]   # torchrun: one device per process
+    with pytest.raises(ValueError, match="only 1 CUDA devices"):
+        resolve_devices(2, 1)
+    with pytest.raises(ValueError, match="no visible device"):
+        resolve_devices(2, 1, world=2, local_rank=1)
+
+
+def test_run_per_device_times_the_slowest_and_keeps_order():
+    import time as _t
+
+    from paper_2009_05534_b200.shard import run_per_device
+    seen = []
+    dt, out = run_per_device(4, lambda i: (_t.sleep(0.02 * (i == 2)), i * i)[1], setup=seen.append)
+    assert out == [0, 1, 4, 9] and sorted(seen) == [0, 1, 2, 3]
+    assert dt >= 0.02
+    with pytest.raises(RuntimeError, match="boom"):
+        run_per_device(3, lambda i: (_ for _ in ()).throw(RuntimeError("boom")) if i == 1 else i)
+
+
+def test_four_standin_devices_match_single_decode():
+    """N=4 in one process (the bench's --gpus 4 path without torchrun): four
+    stand-in device plans, shards merged in order == one decode."""
+    from paper_2009_05534_b200.shard import MultiDeviceDecoder, resolve_devices
+
+    bg = nr.load_basegraph("BG1", 16)
+    cfg = nr.DecodeConfig(max_iter=5, early_stop="none")
+    _, llr = noisy_llrs(bg, bg.m_bg, 1.5, 13, seed=(4, 4))
+    blocks = oracle.quantize_i8(llr, 16)
+    devices = resolve_devices(4, 4)
+    dec = MultiDeviceDecoder(bg, bg.m_bg, cfg, devices=devices, plan_factory=lambda d: _OraclePlan(bg, cfg))
+    try:
+        res = dec.decode(blocks)
+    finally:
+        dec.close()
+    ref = oracle.decode(blocks, bg, cfg)
+    assert np.array_equal(res.bits, ref["bits"]) and np.array_equal(res.iterations, ref["iterations"])
