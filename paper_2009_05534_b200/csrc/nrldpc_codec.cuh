@@ -21,6 +21,8 @@ struct EncSched {
   int row[4], col[4], shift[4];
 };
 
+// Non-template kernels: compiled only in the TU that launches them.
+#ifdef NRLDPC_AUX_KERNELS
 // One codeword per CTA, Z threads; x holds one byte per codeword bit.
 __global__ void __launch_bounds__(512) k_encode(const __grid_constant__ KParams p, EncSched es,
                                                 const uint8_t* __restrict__ msgs, long long batch,
@@ -135,5 +137,7 @@ __global__ void __launch_bounds__(256) k_channel_awgn(const uint8_t* __restrict_
     }
   }
 }
+
+#endif  // NRLDPC_AUX_KERNELS
 
 }  // namespace nr

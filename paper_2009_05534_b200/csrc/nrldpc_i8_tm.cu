@@ -1,0 +1,18 @@
+// int8 decode, TM layout (tensor-memory message rows): its own translation
+// unit so the kernel instantiations compile in parallel.
+#include "nrldpc_launch.cuh"
+
+cudaError_t launch_int8_tm(const nrldpc_plan* plan, Shape& sh, const int8_t* in, int64_t batch, const KOut& o,
+                           cudaStream_t st, bool refill) {
+  const int dev = plan->device;
+  if (refill && (in == nullptr || batch > 2)) {
+    cudaError_t e;
+    if (sh.nreg == 6) e = launch_refill<1, 19, 6, true>(sh, dev, in, batch, o, st);
+    else if (plan->schedule == 1) e = launch_refill<1, 19, 0, true>(sh, dev, in, batch, o, st);
+    else e = launch_refill<2, 10, 0, true>(sh, dev, in, batch, o, st);
+    if (in != nullptr || e != cudaSuccess) return e;
+  }
+  if (sh.nreg == 6) return launch_i8<1, 19, 2, 6, true, true>(sh, dev, in, batch, o, st);
+  if (plan->schedule == 1) return launch_i8<1, 19, 2, 0, true, true>(sh, dev, in, batch, o, st);
+  return launch_i8<2, 10, 2, 0, true, true>(sh, dev, in, batch, o, st);
+}

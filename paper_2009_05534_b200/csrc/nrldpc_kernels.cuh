@@ -114,14 +114,46 @@ __device__ __forceinline__ uint32_t pack_elem(half2 h) {
   return LANES == 2 ? __byte_perm(h2u(h), 0, 0x0020) : h2u(h);
 }
 
+// ---- checked build (NRLDPC_CHECKED, libnrldpc_checked.so) ------------------
+// compute-sanitizer is not available on the GPU pool, so the checked build
+// carries its own device-side checks: every shared-memory access through the
+// helpers below must fall inside the CTA's dynamic shared memory and be
+// naturally aligned; every tensor-memory access must stay in the executing
+// warp's lane quarter and below column 512; result writes must index a
+// codeword of the batch (NR_CHECK at the call sites). A violation traps.
+#ifdef NRLDPC_CHECKED
+extern __shared__ __align__(16) uint8_t nr_chk_dyn_smem[];
+__device__ __forceinline__ void chk_smem(uint32_t a, uint32_t n) {
+  uint32_t dyn;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(nr_chk_dyn_smem);
+  if (a < base || a + n > base + dyn || (a & (n - 1)) != 0) __trap();
+}
+__device__ __forceinline__ void chk_tmem(uint32_t a, uint32_t n) {
+  if ((a >> 16) != 32u * ((threadIdx.x >> 5) & 3u) || (a & 0xFFFFu) + n > 512u) __trap();
+}
+#define NR_CHECK(c)       \
+  do {                    \
+    if (!(c)) __trap();   \
+  } while (0)
+#else
+__device__ __forceinline__ void chk_smem(uint32_t, uint32_t) {}
+__device__ __forceinline__ void chk_tmem(uint32_t, uint32_t) {}
+#define NR_CHECK(c) \
+  do {              \
+  } while (0)
+#endif
+
 template <int LANES>
 __device__ __forceinline__ uint32_t ld_elem(const uint8_t* p) {
+  chk_smem((uint32_t)__cvta_generic_to_shared(p), LANES);
   if (LANES == 2) return *reinterpret_cast<const uint16_t*>(p);
   return *p;
 }
 
 template <int LANES>
 __device__ __forceinline__ void st_elem(uint8_t* p, uint32_t v) {
+  chk_smem((uint32_t)__cvta_generic_to_shared(p), LANES);
   if (LANES == 2) *reinterpret_cast<uint16_t*>(p) = (uint16_t)v;
   else *p = (uint8_t)v;
 }
@@ -133,6 +165,7 @@ __device__ __forceinline__ void st_elem(uint8_t* p, uint32_t v) {
 template <int LANES>
 __device__ __forceinline__ void st_elem_if(uint8_t* p, uint32_t v, bool ok) {
   const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+  chk_smem(a, LANES);
   if (LANES == 2)
     asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.u16 [%0], %1; }" ::"r"(a), "h"((uint16_t)v),
                  "r"((uint32_t)ok));
@@ -147,6 +180,7 @@ __device__ __forceinline__ void st_elem_if(uint8_t* p, uint32_t v, bool ok) {
 // volatile keeps NVVM from moving the loads across barriers.
 template <int LANES>
 __device__ __forceinline__ uint32_t lds_elem(uint32_t a) {
+  chk_smem(a, LANES);
   uint16_t v;
   if (LANES == 2)
     asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
@@ -157,6 +191,7 @@ __device__ __forceinline__ uint32_t lds_elem(uint32_t a) {
 
 template <int LANES>
 __device__ __forceinline__ void sts_elem_if(uint32_t a, uint32_t v, bool ok) {
+  chk_smem(a, LANES);
   if (LANES == 2)
     asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.u16 [%0], %1; }" ::"r"(a), "h"((uint16_t)v),
                  "r"((uint32_t)ok));
@@ -166,25 +201,30 @@ __device__ __forceinline__ void sts_elem_if(uint32_t a, uint32_t v, bool ok) {
 }
 
 __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  chk_smem(a, 4);
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
 
 __device__ __forceinline__ void sts_u32_if(uint32_t a, uint32_t v, bool ok) {
+  chk_smem(a, 4);
   asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.u32 [%0], %1; }" ::"r"(a), "r"(v),
                "r"((uint32_t)ok));
 }
 
 __device__ __forceinline__ void lds_v2(uint32_t a, uint32_t& x, uint32_t& y) {
+  chk_smem(a, 8);
   asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(x), "=r"(y) : "r"(a));
 }
 
 __device__ __forceinline__ void sts_v2(uint32_t a, uint32_t x, uint32_t y) {
+  chk_smem(a, 8);
   asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y));
 }
 
 __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+  chk_smem(a, 4);
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v));
 }
 
@@ -194,23 +234,29 @@ __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
 // (lane quarter in bits 31:16, column in bits 15:0) and the instructions are
 // warp-collective. A row of W messages is one x4 plus an x2 / x1 remainder.
 __device__ __forceinline__ void tm_ld1(uint32_t a, uint32_t& r0) {
+  chk_tmem(a, 1);
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r0) : "r"(a));
 }
 __device__ __forceinline__ void tm_ld2(uint32_t a, uint32_t& r0, uint32_t& r1) {
+  chk_tmem(a, 2);
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(a));
 }
 __device__ __forceinline__ void tm_ld4(uint32_t a, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  chk_tmem(a, 4);
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                : "r"(a));
 }
 __device__ __forceinline__ void tm_st1(uint32_t a, uint32_t r0) {
+  chk_tmem(a, 1);
   asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(a), "r"(r0));
 }
 __device__ __forceinline__ void tm_st2(uint32_t a, uint32_t r0, uint32_t r1) {
+  chk_tmem(a, 2);
   asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(a), "r"(r0), "r"(r1));
 }
 __device__ __forceinline__ void tm_st4(uint32_t a, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
+  chk_tmem(a, 4);
   asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(r0), "r"(r1),
                "r"(r2), "r"(r3));
 }

@@ -40,6 +40,11 @@ class MixedBatchDecoder:
         self.inputs = [torch.zeros((g.batch, p.n_c), dtype=dtype, device=dev)
                        for g, p in zip(groups, self.plans)]
         self.outputs = [p.alloc_outputs(g.batch) for g, p in zip(groups, self.plans)]
+        # one status word for the whole batch (any group's int8 -128 flags it):
+        # a single memset per replay instead of one per group
+        self._status = torch.zeros(1, dtype=torch.int32, device=dev)
+        for out in self.outputs:
+            out["status"] = self._status
         self._streams = [torch.cuda.Stream(device=dev) for _ in range(max(1, streams))]
         self._order = self._schedule(len(self._streams))
         self._graph = None
@@ -71,9 +76,8 @@ class MixedBatchDecoder:
     def _launch_all(self):
         import torch
         cur = torch.cuda.current_stream(self._device)
-        # the status words (int8 -128 seen) restart at zero on every replay
-        for out in self.outputs:
-            out["status"].zero_()
+        # the status word (int8 -128 seen) restarts at zero on every replay
+        self._status.zero_()
         for s in self._streams:
             s.wait_stream(cur)
         for i, si in self._order:
@@ -123,9 +127,8 @@ class MixedBatchDecoder:
             x.copy_(t)
         self.replay()
         results = []
-        for plan, out in zip(self.plans, self.outputs):
-            if int(out["status"].item()):  # synchronizes with the replay
-                raise ValueError("int8 LLR magnitudes must be at most 127")
+        if int(self._status.item()):  # synchronizes with the replay
+            raise ValueError("int8 LLR magnitudes must be at most 127")
         for plan, out in zip(self.plans, self.outputs):
             h = {k: v.cpu().numpy() for k, v in out.items() if k in ("bits", "iters", "synd", "success", "crc_ok")}
             results.append(DecodeResult(

@@ -63,4 +63,6 @@ def main(which):
 
 
 if __name__ == "__main__":
+    from paper_2009_05534_b200 import _native
+    print("library:", _native.LIB_PATH.name)
     main(sys.argv[1:] or ["pair", "tm", "refill", "float", "quant"])
