@@ -17,6 +17,7 @@
 #include <atomic>
 #include <condition_variable>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -522,32 +523,51 @@ static cudaError_t launch_shape(const nrldpc_plan* plan, Shape& sh, const int8_t
 // of the PCIe DMA it feeds. NRLDPC_HOST_THREADS overrides the size.
 class HostPool {
  public:
+  // One parallel job: f(i) for i in [0, n), tasks handed out in index order.
+  struct Job {
+    std::function<void(int)> f;
+    int n = 0;
+    std::atomic<int> next{0}, left{0};
+  };
   static HostPool& get() {
     static HostPool pool;
     return pool;
   }
-  int size() const { return (int)workers_.size() + 1; }
-  // f(i) for i in [0, n): the caller runs tasks too; returns when all done
-  void run(int n, const std::function<void(int)>& f) {
+  int workers() const { return (int)workers_.size(); }
+  // Start a job on the worker threads and return at once; the caller may do
+  // other work (e.g. issue DMAs as pieces complete) before wait(). One job
+  // at a time: submit holds the pool until the matching wait.
+  std::shared_ptr<Job> submit(int n, std::function<void(int)> f) {
+    auto job = std::make_shared<Job>();
+    job->f = std::move(f);
+    job->n = n;
+    job->left.store(n);
+    call_mu_.lock();
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = job;
+      ++gen_;
+    }
+    cv_.notify_all();
+    return job;
+  }
+  // The caller helps with the remaining tasks, then waits for the job.
+  void wait(const std::shared_ptr<Job>& job) {
+    work(*job);
+    {
+      std::unique_lock<std::mutex> lk(mu_);
+      done_cv_.wait(lk, [&] { return job->left.load() == 0; });
+      job_.reset();
+    }
+    call_mu_.unlock();
+  }
+  void run(int n, std::function<void(int)> f) {
     if (n <= 0) return;
     if (n == 1 || workers_.empty()) {
       for (int i = 0; i < n; ++i) f(i);
       return;
     }
-    std::unique_lock<std::mutex> call(call_mu_);  // one parallel job at a time
-    {
-      std::lock_guard<std::mutex> lk(mu_);
-      job_ = &f;
-      n_ = n;
-      next_.store(0);
-      left_.store(n);
-      ++gen_;
-    }
-    cv_.notify_all();
-    work();
-    std::unique_lock<std::mutex> lk(mu_);
-    done_cv_.wait(lk, [&] { return left_.load() == 0; });
-    job_ = nullptr;
+    wait(submit(n, std::move(f)));
   }
 
  private:
@@ -555,7 +575,7 @@ class HostPool {
     int n = (int)std::thread::hardware_concurrency();
     if (const char* e = std::getenv("NRLDPC_HOST_THREADS")) n = std::atoi(e);
     n = std::max(1, std::min(n, 8));
-    for (int i = 0; i + 1 < n; ++i) workers_.emplace_back([this] { loop(); });
+    for (int i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
   }
   ~HostPool() {
     {
@@ -566,12 +586,12 @@ class HostPool {
     cv_.notify_all();
     for (auto& t : workers_) t.join();
   }
-  void work() {
+  void work(Job& job) {
     for (;;) {
-      const int i = next_.fetch_add(1);
-      if (i >= n_) return;
-      (*job_)(i);
-      if (left_.fetch_sub(1) == 1) {
+      const int i = job.next.fetch_add(1);
+      if (i >= job.n) return;
+      job.f(i);
+      if (job.left.fetch_sub(1) == 1) {
         std::lock_guard<std::mutex> lk(mu_);
         done_cv_.notify_all();
       }
@@ -580,36 +600,35 @@ class HostPool {
   void loop() {
     uint64_t seen = 0;
     for (;;) {
+      std::shared_ptr<Job> job;
       {
         std::unique_lock<std::mutex> lk(mu_);
         cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
         if (stop_) return;
         seen = gen_;
-        if (!job_) continue;
+        job = job_;
       }
-      work();
+      if (job) work(*job);
     }
   }
   std::vector<std::thread> workers_;
   std::mutex mu_, call_mu_;
   std::condition_variable cv_, done_cv_;
-  const std::function<void(int)>* job_ = nullptr;
-  int n_ = 0;
-  std::atomic<int> next_{0}, left_{0};
+  std::shared_ptr<Job> job_;
   uint64_t gen_ = 0;
   bool stop_ = false;
 };
 
 static void host_copy(void* dst, const void* src, size_t n) {
-  constexpr size_t kPiece = 1u << 20;
+  constexpr size_t kPiece = 256u << 10;
   HostPool& pool = HostPool::get();
-  const int parts = (int)std::min<size_t>((size_t)pool.size(), (n + kPiece - 1) / kPiece);
+  const int parts = (int)std::min<size_t>((size_t)pool.workers() + 1, (n + kPiece - 1) / kPiece);
   if (parts <= 1) {
     std::memcpy(dst, src, n);
     return;
   }
   const size_t per = ((n + parts - 1) / parts + 4095) & ~size_t(4095);
-  pool.run(parts, [&](int i) {
+  pool.run(parts, [=](int i) {
     const size_t o = (size_t)i * per;
     if (o < n) std::memcpy(static_cast<uint8_t*>(dst) + o, static_cast<const uint8_t*>(src) + o, std::min(per, n - o));
   });
@@ -794,7 +813,8 @@ int nrldpc_unpack_bits(const uint32_t* words, int64_t batch, int64_t words_per_c
     return t;
   }();
   HostPool& pool = HostPool::get();
-  const int64_t per = std::max<int64_t>(1, (batch + 4 * pool.size() - 1) / (4 * pool.size()));
+  const int nt = pool.workers() + 1;
+  const int64_t per = std::max<int64_t>(1, (batch + 4 * nt - 1) / (4 * nt));
   const int parts = (int)((batch + per - 1) / per);
   pool.run(parts, [&](int part) {
     const int64_t c0 = part * per, c1 = std::min(batch, c0 + per);
@@ -1268,6 +1288,11 @@ static int host_enqueue(nrldpc_plan* plan, int si, const void* llr_host, int64_t
     const int64_t nb = std::min<int64_t>(chunk, batch - b0);
     const uint8_t* src = static_cast<const uint8_t*>(llr_host) + b0 * per_cw_in;
     if (stage_in) {
+      // host copy of this chunk on the pool (the DMA of the previous chunk
+      // runs meanwhile). Measured on the GPU box: the staging is bound by
+      // host memory bandwidth (copy read + write + the DMA's read); letting
+      // the copy run ahead of the DMA on all workers was slower (2.0 vs
+      // 1.3 ms per 26.7 MB batch, tools/api_phase_probe.py)
       host_copy(sl.h_in + b0 * per_cw_in, src, nb * per_cw_in);
       src = sl.h_in + b0 * per_cw_in;
     }

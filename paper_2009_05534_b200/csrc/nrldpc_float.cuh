@@ -63,8 +63,21 @@ struct FOps<NRLDPC_F16> {
   __device__ static uint32_t minv(uint32_t a, uint32_t b) { return h2u(__hmin2(u2h(a), u2h(b))); }
   __device__ static uint32_t maxv(uint32_t a, uint32_t b) { return h2u(__hmax2(u2h(a), u2h(b))); }
   __device__ static uint32_t mul(uint32_t a, uint32_t b) { return h2u(__hmul2(u2h(a), u2h(b))); }
-  __device__ static uint32_t neg_mask(uint32_t a) { return __hlt2_mask(u2h(a), u2h(0u)); }
-  __device__ static uint32_t eq_mask(uint32_t a, uint32_t b) { return __heq2_mask(u2h(a), u2h(b)); }
+  // a < 0 per lane (-0 is not negative) in the lane's sign bit only, which is
+  // all the callers read (sign products, parity bits 15/31): sign bit AND a
+  // nonzero magnitude. |a| + 0x7FFF sets bit 15 exactly when |a| != 0 and
+  // cannot carry into the other lane (|a| <= 0x7C00). Integer ops instead of
+  // HSET2, which issues at a quarter of the full rate on sm_100.
+  __device__ static uint32_t neg_mask(uint32_t a) { return a & ((a & 0x7FFF7FFFu) + 0x7FFF7FFFu) & sign; }
+  // a == b per lane as a full-lane mask, for non-negative a and b (|t| and
+  // m1): equal halves have equal bits, so a ^ b is zero exactly there; the
+  // same carry-free test marks nonzero lanes in bit 15, and PRMT replicates
+  // that bit over the lane (0xbb99: the sign bits of bytes 1 and 3)
+  __device__ static uint32_t eq_mask(uint32_t a, uint32_t b) {
+    uint32_t ne;
+    asm("prmt.b32 %0, %1, 0, 0xbb99;" : "=r"(ne) : "r"((a ^ b) + 0x7FFF7FFFu));
+    return ~ne;
+  }
   __device__ static float lane_abs(uint32_t a, int l) {
     return fabsf(__half2float(l ? __high2half(u2h(a)) : __low2half(u2h(a))));
   }
@@ -80,6 +93,46 @@ struct FOps<NRLDPC_F16> {
 template <int BG>
 __host__ __device__ constexpr int ftm_kind(int w) {
   return BG == 1 ? (w == 19 ? 0 : w >= 7 ? 1 : 2) : (w >= 8 ? 1 : 2);
+}
+
+// Two smallest of a[0..W-1] (non-negative, NaN-free) from the fold identity
+// F::sat(), as a pairwise tree (see two_smallest in nrldpc_device.cuh).
+template <typename F, int N>
+__device__ __forceinline__ void flt_merge(uint32_t (&lo)[N], uint32_t (&hi)[N]) {
+  if constexpr (N > 1) {
+    constexpr int M = (N + 1) / 2;
+    uint32_t nlo[M], nhi[M];
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) {
+      nlo[i] = F::minv(lo[2 * i], lo[2 * i + 1]);
+      nhi[i] = F::minv(F::minv(F::maxv(lo[2 * i], lo[2 * i + 1]), hi[2 * i]), hi[2 * i + 1]);
+    }
+    if constexpr ((N & 1) != 0) {
+      nlo[M - 1] = lo[N - 1];
+      nhi[M - 1] = hi[N - 1];
+    }
+    flt_merge<F, M>(nlo, nhi);
+    lo[0] = nlo[0];
+    hi[0] = nhi[0];
+  }
+}
+
+template <typename F, int W>
+__device__ __forceinline__ void flt_two_smallest(const uint32_t (&a)[W], uint32_t& m1, uint32_t& m2) {
+  constexpr int P = (W + 1) / 2;
+  uint32_t lo[P], hi[P];
+#pragma unroll
+  for (int i = 0; i < W / 2; ++i) {
+    lo[i] = F::minv(a[2 * i], a[2 * i + 1]);
+    hi[i] = F::maxv(a[2 * i], a[2 * i + 1]);
+  }
+  if constexpr ((W & 1) != 0) {
+    lo[P - 1] = a[W - 1];
+    hi[P - 1] = F::sat();
+  }
+  flt_merge<F, P>(lo, hi);
+  m1 = F::minv(lo[0], F::sat());
+  m2 = F::minv(hi[0], F::sat());
 }
 
 // One row of a compile-time (BG1/BG2) layer unit in the float engines,
@@ -117,19 +170,20 @@ struct FRow {
   }
   __device__ __forceinline__ void main(const uint8_t* Lg, uint32_t beta) {
     if constexpr (KIND == 2) tm_wait_ld<W>(msg);
-    m1 = F::sat();
-    m2 = F::sat();
     S = 0;
+    uint32_t a[W];
 #pragma unroll
     for (int j = 0; j < W; ++j) {
       const uint32_t lv = *reinterpret_cast<const uint32_t*>(Lg + off[j]);
       t[j] = F::sub_clamp(lv, msg[j]);             // decoder.py:300
-      const uint32_t a = F::absv(t[j]);
+      a[j] = F::absv(t[j]);
       neg[j] = F::neg_mask(t[j]);                  // lvc < 0 (-0 is not negative)
-      m2 = F::minv(m2, F::maxv(m1, a));            // kernels.py:247-250
-      m1 = F::minv(m1, a);
       S ^= neg[j];
     }
+    // the two smallest |t| (kernels.py:247-250 fold from the saturation
+    // identity) as a pairwise tree: the same values as the sequential fold
+    // (ties give m1 == m2 either way), ~log2(W) deep instead of ~2W
+    flt_two_smallest<F, W>(a, m1, m2);
     b1 = F::mul(beta, m1);                         // dtype(beta) * m
     b2 = F::mul(beta, m2);
   }
