@@ -131,6 +131,22 @@ int nrldpc_decode(nrldpc_plan* plan, const void* llr, int64_t batch,
                   float* trace_m, int32_t* status, void* stream);
 
 /*
+ * Mixed-size batches (BASELINE config 4; transport-block segmentation): one
+ * launch decodes up to NRLDPC_MULTI_MAX groups, each with its own plan
+ * (graph, Z, rows_used), when the plans share a kernel variant and CTA size
+ * (nrldpc_plan_kernel). Same semantics per group as nrldpc_decode without a
+ * trace; device pointers; one shared status word (may be NULL); crc_ok may
+ * be NULL unless the plans are in crc mode. Many small per-shape launches
+ * are limited by how many kernels run concurrently, not by their work; this
+ * packs up to five shapes into one grid.
+ */
+#define NRLDPC_MULTI_MAX 5
+int nrldpc_plan_kernel(const nrldpc_plan* plan, int* kernel, int* threads, int64_t* smem_bytes);
+int nrldpc_decode_multi(nrldpc_plan* const* plans, int n, const void* const* llr, const int64_t* batch,
+                        uint32_t* const* bits, int32_t* const* iters, int32_t* const* synd,
+                        uint8_t* const* success, uint8_t* const* crc_ok, int32_t* status, void* stream);
+
+/*
  * Flooding-schedule decode (decoder.py:337-365, 569-581): every row reads the
  * previous iteration's posteriors, then L = sat(L_b + sum of messages).
  * Same buffers, status word and early-stop semantics as nrldpc_decode

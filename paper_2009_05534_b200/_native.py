@@ -22,6 +22,7 @@ INT8, F16, F32 = 0, 1, 2
 STOP_SYNDROME, STOP_CRC, STOP_NONE = 0, 1, 2
 CRC_KINDS = {"crc24a": 0, "crc24b": 1, "crc16": 2}
 IN_F64, IN_F32 = 0, 1
+MULTI_MAX = 5  # NRLDPC_MULTI_MAX
 
 # every symbol include/nrldpc.h declares (checked by tests/test_abi.py)
 EXPORTS = (
@@ -36,6 +37,8 @@ EXPORTS = (
     "nrldpc_decode_host_async",
     "nrldpc_host_wait",
     "nrldpc_decode_flooding",
+    "nrldpc_plan_kernel",
+    "nrldpc_decode_multi",
     "nrldpc_encode",
     "nrldpc_channel_awgn",
     "nrldpc_unpack_bits",
@@ -93,6 +96,10 @@ def load() -> ctypes.CDLL:
     lib.nrldpc_host_wait.restype = c_int
     lib.nrldpc_decode_flooding.argtypes = [c_void_p, c_void_p, c_int64] + [c_void_p] * 9
     lib.nrldpc_decode_flooding.restype = c_int
+    lib.nrldpc_plan_kernel.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p]
+    lib.nrldpc_plan_kernel.restype = c_int
+    lib.nrldpc_decode_multi.argtypes = [c_void_p, c_int, c_void_p, c_void_p] + [c_void_p] * 5 + [c_void_p, c_void_p]
+    lib.nrldpc_decode_multi.restype = c_int
     lib.nrldpc_encode.argtypes = [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]
     lib.nrldpc_encode.restype = c_int
     lib.nrldpc_channel_awgn.argtypes = [c_void_p, c_void_p, c_int64, c_double, c_double,

@@ -515,6 +515,23 @@ static cudaError_t launch_shape(const nrldpc_plan* plan, Shape& sh, const int8_t
   return launch_int8_bg2(plan, sh, in, batch, o, st, refill);
 }
 
+// The int8 kernel instantiation launch_shape would use for `sh` (plain pair
+// kernel, no refill): the grouping key of multi-shape launches. 0: none.
+static int kernel_variant(const nrldpc_plan* plan, const Shape& sh) {
+  if (plan->precision != NRLDPC_INT8 || sh.threads == 0) return 0;
+  const bool two = sh.lanes == 2;
+  if (sh.tm) return sh.nreg == 6 ? 1 : plan->schedule == 1 ? 2 : 3;
+  if (plan->schedule == 1) {
+    if (!two) return 10;
+    if (sh.nreg == 0) return sh.abs ? 11 : 12;
+    if (!sh.abs) return 0;
+    return sh.nreg == 2 ? 13 : sh.nreg == 4 ? 14 : 15;
+  }
+  if (plan->schedule == 2) return !two ? 20 : sh.abs ? 21 : 22;
+  if (plan->maxw > 10) return two ? 30 : 31;
+  return two ? 32 : 33;
+}
+
 // ---- host worker pool -------------------------------------------------------
 // A few persistent threads for the host side of the end-to-end path: copying
 // a pageable caller's input into pinned staging memory, and unpacking packed
@@ -1116,6 +1133,55 @@ int nrldpc_plan_destroy(nrldpc_plan* plan) {
   if (plan->d_crc_tab) cudaFree(plan->d_crc_tab);
   cudaSetDevice(prev);
   delete plan;
+  return NRLDPC_OK;
+}
+
+int nrldpc_plan_kernel(const nrldpc_plan* plan, int* kernel, int* threads, int64_t* smem_bytes) {
+  if (!plan) return fail(NRLDPC_EINVAL, "plan is NULL");
+  if (kernel) *kernel = kernel_variant(plan, plan->main);
+  if (threads) *threads = plan->main.threads;
+  if (smem_bytes) *smem_bytes = (int64_t)plan->main.smem;
+  return NRLDPC_OK;
+}
+
+int nrldpc_decode_multi(nrldpc_plan* const* plans, int n, const void* const* llr, const int64_t* batch,
+                        uint32_t* const* bits, int32_t* const* iters, int32_t* const* synd,
+                        uint8_t* const* success, uint8_t* const* crc_ok, int32_t* status, void* stream) {
+  g_launches = 0;
+  if (!plans || !llr || !batch || !bits || !iters || !synd || !success)
+    return fail(NRLDPC_EINVAL, "NULL array");
+  if (n < 1 || n > NRLDPC_MULTI_MAX) return fail(NRLDPC_EINVAL, "n must be in [1, NRLDPC_MULTI_MAX]");
+  const nrldpc_plan* p0 = plans[0];
+  if (!p0) return fail(NRLDPC_EINVAL, "plan is NULL");
+  const int kern = kernel_variant(p0, p0->main);
+  if (kern == 0) return fail(NRLDPC_EINVAL, "multi-shape launches need int8 plans");
+  Shape* sh[kMultiShapes];
+  const int8_t* in[kMultiShapes];
+  long long nb[kMultiShapes];
+  KOut o[kMultiShapes];
+  for (int i = 0; i < n; ++i) {
+    nrldpc_plan* p = plans[i];
+    if (!p) return fail(NRLDPC_EINVAL, "plan is NULL");
+    if (p->device != p0->device) return fail(NRLDPC_EINVAL, "plans of one multi-shape launch share a device");
+    if (kernel_variant(p, p->main) != kern || p->main.threads != p0->main.threads)
+      return fail(NRLDPC_EINVAL, "plans of one multi-shape launch need the same kernel variant and CTA size");
+    if (batch[i] < 0) return fail(NRLDPC_EINVAL, "batch must be non-negative");
+    if (batch[i] > 0 && (!llr[i] || !bits[i] || !iters[i] || !synd[i] || !success[i]))
+      return fail(NRLDPC_EINVAL, "NULL buffer");
+    if (p->early_stop == NRLDPC_STOP_CRC && batch[i] > 0 && (!crc_ok || !crc_ok[i]))
+      return fail(NRLDPC_EINVAL, "crc mode needs a crc_ok buffer");
+    sh[i] = &p->main;
+    in[i] = static_cast<const int8_t*>(llr[i]);
+    nb[i] = batch[i];
+    o[i] = KOut{bits[i], iters[i], synd[i], success[i], crc_ok ? crc_ok[i] : nullptr, nullptr, nullptr, status,
+                nullptr};
+  }
+  NR_CUDA(cudaSetDevice(p0->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const cudaError_t e = kern <= 3    ? launch_int8_multi_tm(kern, sh, n, in, nb, o, p0->device, st)
+                        : kern < 20  ? launch_int8_multi_bg1(kern, sh, n, in, nb, o, p0->device, st)
+                                     : launch_int8_multi_bg2(kern, sh, n, in, nb, o, p0->device, st);
+  if (e != cudaSuccess) return cuda_fail(e, "multi-shape decode launch");
   return NRLDPC_OK;
 }
 

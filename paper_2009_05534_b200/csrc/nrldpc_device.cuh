@@ -1149,8 +1149,8 @@ __device__ __forceinline__ uint32_t crc_partial(const KParams& p, const uint8_t*
 // clamp but never store, so the layer loop runs warp-uniform and the graph
 // tables stay in uniform registers.
 template <int BG, int MAXW, int LANES, int NREG, bool ABS, bool TM = false>
-__global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_constant__ KParams p,
-                                                                   const int8_t* __restrict__ llr, KOut o) {
+__device__ __forceinline__ void decode_i8_cta(const KParams& p, const int8_t* __restrict__ llr, const KOut o,
+                                              const long long cta_idx) {
   static_assert(NREG == 0 || (BG == 1 && LANES == 2), "register messages: BG1 pairs only");
   static_assert(!ABS || BG != 0, "absolute addressing: compile-time schedules only");
   static_assert(!TM || (BG != 0 && LANES == 2 && (NREG == 6 || NREG == 0) && ABS), "TM layout: pair shapes");
@@ -1167,7 +1167,7 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
   const bool st_ok = NREG > 0 || tid < p.groups * p.z;
   const int g = st_ok ? tid / p.z : p.groups - 1;
   const int z = st_ok ? tid - g * p.z : (tid - g * p.z) % p.z;
-  const long long cw0 = ((long long)blockIdx.x * p.groups + g) * LANES;
+  const long long cw0 = (cta_idx * p.groups + g) * LANES;
   const bool active = st_ok && cw0 < p.batch;        // owns real codewords
   const uint32_t ZL = (uint32_t)p.z * ES;
   const uint32_t zl = (uint32_t)z * ES;
@@ -1183,7 +1183,7 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
 
   for (int i = tid; i < 128; i += blockDim.x) lut[i] = p.lut[i];
   if (tid == 0) {
-    const long long first = (long long)blockIdx.x * p.groups * LANES;
+    const long long first = cta_idx * p.groups * LANES;
     const long long rem = p.batch - first;
     cta->n_done = 0;
     cta->n_valid = (int)min(rem, (long long)p.groups * LANES);
@@ -1452,6 +1452,30 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_
     __syncthreads();
     if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(lds_u32(&cta->kc[5])));
   }
+}
+
+// One launch, one shape: CTA blockIdx.x decodes codewords
+// [blockIdx.x * groups * LANES, ...).
+template <int BG, int MAXW, int LANES, int NREG, bool ABS, bool TM = false>
+__global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8(const __grid_constant__ KParams p,
+                                                                   const int8_t* __restrict__ llr, KOut o) {
+  decode_i8_cta<BG, MAXW, LANES, NREG, ABS, TM>(p, llr, o, (long long)blockIdx.x);
+}
+
+// One launch, up to kMultiShapes shapes of the same kernel variant and CTA
+// size (mixed-size batches, BASELINE config 4): shape s owns CTAs
+// [cta_end[s-1], cta_end[s]). Each shape's full KParams sits in the
+// parameter block, so its graph tables are read from the constant bank with
+// a uniform shape offset, exactly as in the one-shape launch. This replaces
+// per-shape launches whose number, not their work, limited a mixed batch:
+// a CUDA-graph replay runs about 32 kernels concurrently (tools/cfg4_probe.py).
+template <int BG, int MAXW, int LANES, int NREG, bool ABS, bool TM = false>
+__global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_multi(const __grid_constant__ KMulti P) {
+  int s = 0;  // block-uniform
+#pragma unroll
+  for (int i = 0; i + 1 < kMultiShapes; ++i) s += (i + 1 < P.n && (int)blockIdx.x >= P.cta_end[i]) ? 1 : 0;
+  const int begin = s ? P.cta_end[s - 1] : 0;
+  decode_i8_cta<BG, MAXW, LANES, NREG, ABS, TM>(P.s[s], P.llr[s], P.o[s], (long long)blockIdx.x - begin);
 }
 
 // ---- lane-refill decode (early-stop modes) --------------------------------

@@ -125,6 +125,14 @@ cudaError_t launch_int8_bg1(const nrldpc_plan* plan, Shape& sh, const int8_t* in
                             cudaStream_t st, bool refill);
 cudaError_t launch_int8_bg2(const nrldpc_plan* plan, Shape& sh, const int8_t* in, int64_t batch, const KOut& o,
                             cudaStream_t st, bool refill);
+// Several shapes of one int8 kernel variant in one launch (mixed batches):
+// `kernel` is the variant id (kernel_variant() in nrldpc.cu).
+cudaError_t launch_int8_multi_tm(int kernel, Shape* const* sh, int n, const int8_t* const* llr,
+                                 const long long* batch, const KOut* o, int device, cudaStream_t st);
+cudaError_t launch_int8_multi_bg1(int kernel, Shape* const* sh, int n, const int8_t* const* llr,
+                                  const long long* batch, const KOut* o, int device, cudaStream_t st);
+cudaError_t launch_int8_multi_bg2(int kernel, Shape* const* sh, int n, const int8_t* const* llr,
+                                  const long long* batch, const KOut* o, int device, cudaStream_t st);
 // float engines (Precision.F16 / F32)
 cudaError_t launch_float_any(int precision, int schedule, Shape& sh, int device, const void* llr, long long batch,
                              const KOut& o, cudaStream_t st);

@@ -19,3 +19,17 @@ cudaError_t launch_int8_bg2(const nrldpc_plan* plan, Shape& sh, const int8_t* in
     return two ? launch_i8<0, 19, 2>(sh, dev, in, batch, o, st) : launch_i8<0, 19, 1>(sh, dev, in, batch, o, st);
   return two ? launch_i8<0, 10, 2>(sh, dev, in, batch, o, st) : launch_i8<0, 10, 1>(sh, dev, in, batch, o, st);
 }
+
+cudaError_t launch_int8_multi_bg2(int kernel, Shape* const* sh, int n, const int8_t* const* llr, const long long* batch,
+                                  const KOut* o, int device, cudaStream_t st) {
+  switch (kernel) {
+    case 20: return launch_i8_multi<2, 10, 1>(sh, n, llr, batch, o, device, st);
+    case 21: return launch_i8_multi<2, 10, 2, 0, true>(sh, n, llr, batch, o, device, st);
+    case 22: return launch_i8_multi<2, 10, 2>(sh, n, llr, batch, o, device, st);
+    case 30: return launch_i8_multi<0, 19, 2>(sh, n, llr, batch, o, device, st);
+    case 31: return launch_i8_multi<0, 19, 1>(sh, n, llr, batch, o, device, st);
+    case 32: return launch_i8_multi<0, 10, 2>(sh, n, llr, batch, o, device, st);
+    case 33: return launch_i8_multi<0, 10, 1>(sh, n, llr, batch, o, device, st);
+    default: return cudaErrorInvalidValue;
+  }
+}

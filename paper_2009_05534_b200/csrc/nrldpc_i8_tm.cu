@@ -16,3 +16,13 @@ cudaError_t launch_int8_tm(const nrldpc_plan* plan, Shape& sh, const int8_t* in,
   if (plan->schedule == 1) return launch_i8<1, 19, 2, 0, true, true>(sh, dev, in, batch, o, st);
   return launch_i8<2, 10, 2, 0, true, true>(sh, dev, in, batch, o, st);
 }
+
+cudaError_t launch_int8_multi_tm(int kernel, Shape* const* sh, int n, const int8_t* const* llr, const long long* batch,
+                                 const KOut* o, int device, cudaStream_t st) {
+  switch (kernel) {
+    case 1: return launch_i8_multi<1, 19, 2, 6, true, true>(sh, n, llr, batch, o, device, st);
+    case 2: return launch_i8_multi<1, 19, 2, 0, true, true>(sh, n, llr, batch, o, device, st);
+    case 3: return launch_i8_multi<2, 10, 2, 0, true, true>(sh, n, llr, batch, o, device, st);
+    default: return cudaErrorInvalidValue;
+  }
+}

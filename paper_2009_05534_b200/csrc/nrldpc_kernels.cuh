@@ -92,6 +92,19 @@ struct KOut {
   int32_t* work;  // lane-refill kernel: next-codeword counter (zeroed per launch)
 };
 
+// Several shapes in one decode launch (k_decode_i8_multi): the parameter
+// block holds each shape's KParams (5.8 KB each; kernel parameters are
+// limited to 32 KB), its input and outputs, and its last CTA + 1.
+constexpr int kMultiShapes = 5;
+struct alignas(16) KMulti {
+  KParams s[kMultiShapes];
+  const int8_t* llr[kMultiShapes];
+  KOut o[kMultiShapes];
+  int cta_end[kMultiShapes];
+  int n;
+};
+static_assert(sizeof(KMulti) <= 32764, "kernel parameter block limit");
+
 __device__ __forceinline__ uint32_t h2u(half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 __device__ __forceinline__ half2 u2h(uint32_t u) { return *reinterpret_cast<half2*>(&u); }
 

@@ -2,6 +2,8 @@
 // the int8 translation units.
 #pragma once
 
+#include <cstring>
+
 #include "nrldpc_host.h"
 
 // Launch (or, with llr == nullptr, only prepare: set the smem attribute and
@@ -81,3 +83,42 @@ static cudaError_t launch_refill(Shape& sh, int device, const int8_t* llr, long 
   return e != cudaSuccess ? e : f;
 }
 
+
+// Several shapes of one kernel variant in one launch (k_decode_i8_multi).
+// All shapes share the CTA size; the launch takes the largest shared-memory
+// request among them. Fixed iterations or early stop (pair kernel), no trace.
+template <int BG, int MAXW, int LANES, int NREG = 0, bool ABS = false, bool TM = false>
+static cudaError_t launch_i8_multi(Shape* const* sh, int n, const int8_t* const* llr, const long long* batch,
+                                   const KOut* o, int device, cudaStream_t st) {
+  static bool attr_done[64] = {};
+  auto kern = k_decode_i8_multi<BG, MAXW, LANES, NREG, ABS, TM>;
+  if (!attr_done[device & 63]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    if (e != cudaSuccess) return e;
+    attr_done[device & 63] = true;
+  }
+  if (n < 1 || n > kMultiShapes) return cudaErrorInvalidValue;
+  static thread_local KMulti P;  // 30 KB: kept off the stack
+  std::memset(&P, 0, sizeof(P));
+  size_t smem = 0;
+  long long ctas = 0;
+  for (int i = 0; i < n; ++i) {
+    if (sh[i]->threads != sh[0]->threads) return cudaErrorInvalidValue;
+    KParams& kp = P.s[i];
+    kp = sh[i]->kp;
+    kp.batch = batch[i];
+    kp.trace = 0;
+    kp.vec_load = ((long long)kp.n_blocks * kp.z) % 16 == 0 && ((uintptr_t)llr[i] & 15) == 0;
+    const long long per_cta = (long long)sh[i]->groups * LANES;
+    ctas += (batch[i] + per_cta - 1) / per_cta;
+    P.cta_end[i] = (int)ctas;
+    P.llr[i] = llr[i];
+    P.o[i] = o[i];
+    smem = std::max(smem, sh[i]->smem);
+  }
+  P.n = n;
+  if (ctas == 0) return cudaSuccess;
+  kern<<<(unsigned)ctas, sh[0]->threads, smem, st>>>(P);
+  ++g_launches;
+  return cudaGetLastError();
+}

@@ -32,8 +32,8 @@ def _same(res, ref):
     assert np.array_equal(res.syndrome_weight, ref["syndrome_weight"])
 
 
-@pytest.mark.parametrize("stop", ["none", "syndrome"])
-def test_config4_full_mixed_batch_vs_oracle(cuda_ok, stop):
+@pytest.mark.parametrize("stop,grouped", [("none", True), ("syndrome", True), ("none", False), ("crc", True)])
+def test_config4_full_mixed_batch_vs_oracle(cuda_ok, stop, grouped):
     """BASELINE config 4 at full size: 102 groups of 16 codewords, one mixed
     batch (MixedBatchDecoder), every group bit-exact against the oracle."""
     from paper_2009_05534_b200.mixed import Group, MixedBatchDecoder
@@ -46,11 +46,34 @@ def test_config4_full_mixed_batch_vs_oracle(cuda_ok, stop):
             groups.append(Group(bg, bg.m_bg, 16))
             data.append(oracle.quantize_i8(llr, z))
     assert len(groups) == 102
-    mixed = MixedBatchDecoder(groups, cfg, streams=32)
+    mixed = MixedBatchDecoder(groups, cfg, streams=32, grouped=grouped)
+    if grouped:
+        assert len(mixed.launches) < 40 and sorted(i for lg in mixed.launches for i in lg) == list(range(102))
     for rep in range(2):  # capture, then a replay
         results = mixed.decode(data)
         for g, res, blocks in zip(groups, results, data):
-            _same(res, oracle.decode(blocks, g.bg, cfg))
+            ref = oracle.decode(blocks, g.bg, cfg)
+            _same(res, ref)
+            if stop == "crc":
+                assert np.array_equal(res.crc_ok, ref["crc_ok"])
+
+
+def test_decode_multi_rejects_mixed_variants(cuda_ok):
+    """nrldpc_decode_multi takes only plans of one kernel variant and CTA size."""
+    import ctypes
+    from paper_2009_05534_b200 import _native
+    cfg = nr.DecodeConfig(max_iter=3)
+    a = nr.get_plan(nr.load_basegraph("BG1", 384), 46, cfg, coscheduled=True)
+    b = nr.get_plan(nr.load_basegraph("BG2", 16), 42, cfg, coscheduled=True)
+    P = ctypes.c_void_p * 2
+    outs = [a.alloc_outputs(1), b.alloc_outputs(1)]
+    x = [torch.zeros((1, a.n_c), dtype=torch.int8, device="cuda"), torch.zeros((1, b.n_c), dtype=torch.int8, device="cuda")]
+    rc = _native.load().nrldpc_decode_multi(
+        P(a.handle.value, b.handle.value), 2, P(*[t.data_ptr() for t in x]), (ctypes.c_int64 * 2)(1, 1),
+        P(*[o["bits"].data_ptr() for o in outs]), P(*[o["iters"].data_ptr() for o in outs]),
+        P(*[o["synd"].data_ptr() for o in outs]), P(*[o["success"].data_ptr() for o in outs]), None, None, None)
+    with pytest.raises(ValueError, match="same kernel variant"):
+        _native.check(rc)
 
 
 def test_config5_slot_batch_vs_oracle(cuda_ok):

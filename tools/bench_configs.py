@@ -157,7 +157,7 @@ def config4(peak_ops, reps=30):
             bg = nr.load_basegraph(bg_id, z)
             groups.append(Group(bg, bg.m_bg, 16))
             data.append(gpu_blocks(bg, bg.m_bg, 2.0, 16, (int(bg_id[-1]), z))[1])
-    mixed = MixedBatchDecoder(groups, cfg, streams=32)
+    mixed = MixedBatchDecoder(groups, cfg, streams=24)
     for x, d in zip(mixed.inputs, data):
         x.copy_(d)
     mixed.capture()

@@ -36,26 +36,27 @@ for bg_id in ("BG1", "BG2"):
         bg = nr.load_basegraph(bg_id, z)
         groups.append(Group(bg, bg.m_bg, 16))
 k_total = sum(16 * g.bg.k_b * g.bg.z for g in groups)
-for streams in (8, 16, 32, 64, 102):
-    m = MixedBatchDecoder(groups, cfg, streams=streams)
-    t = replay_ms(m)
-    print(f"streams={streams:3d}: {t:.3f} ms  {k_total / t / 1e6:.2f} Gbps")
-m = MixedBatchDecoder(groups, cfg, streams=32)
+for grouped in (True, False):
+    for streams in (8, 16, 32, 64):
+        m = MixedBatchDecoder(groups, cfg, streams=streams, grouped=grouped)
+        t = replay_ms(m)
+        print(f"grouped={grouped} launches={len(m.launches)} streams={streams:3d}: {t:.3f} ms  "
+              f"{k_total / t / 1e6:.2f} Gbps")
+m = MixedBatchDecoder(groups, cfg, streams=32, grouped=False)
 alone = [g for g, p in zip(groups, m.plans) if p.smem_bytes > 116 * 1024 or p.threads_per_cta >= 384]
 rest = [g for g, p in zip(groups, m.plans) if not (p.smem_bytes > 116 * 1024 or p.threads_per_cta >= 384)]
-print("groups holding an SM alone:", len(alone), "ms", replay_ms(MixedBatchDecoder(alone, cfg, streams=32)))
-print("other groups:", len(rest), "ms", replay_ms(MixedBatchDecoder(rest, cfg, streams=32)))
+print("groups holding an SM alone:", len(alone), "ms", replay_ms(MixedBatchDecoder(alone, cfg, streams=32, grouped=False)))
+print("other groups:", len(rest), "ms", replay_ms(MixedBatchDecoder(rest, cfg, streams=32, grouped=False)))
+print("groups holding an SM alone, grouped:", replay_ms(MixedBatchDecoder(alone, cfg, streams=32)))
+print("other groups, grouped:", replay_ms(MixedBatchDecoder(rest, cfg, streams=32)))
 for g, p in zip(groups, m.plans):
     print(f"  {g.bg.id} Z={g.bg.z:3d} threads={p.threads_per_cta:3d} cw/cta={p.codewords_per_cta} smem={p.smem_bytes}")
 
-print("-- stream sweeps per subset")
-for name, sub in (("small", rest), ("big", alone)):
-    for st in (8, 16, 32, 64, len(sub)):
-        print(f"{name} groups ({len(sub)}), streams={st}: {replay_ms(MixedBatchDecoder(sub, cfg, streams=st)):.3f} ms")
-# small groups first: order by increasing cost instead of LPT
-class SmallFirst(MixedBatchDecoder):
+
+print("-- grouped, stream count and launch order")
+class ShortFirst(MixedBatchDecoder):
     def _schedule(self, n):
-        order = super()._schedule(n)
-        return list(reversed(order))
-for st in (32, 64, 102):
-    print(f"all groups, reversed LPT (short first), streams={st}: {replay_ms(SmallFirst(groups, cfg, streams=st)):.3f} ms")
+        return list(reversed(super()._schedule(n)))
+for st in (20, 24, 28, 32, 33, 40, 48):
+    print(f"grouped LPT streams={st}: {replay_ms(MixedBatchDecoder(groups, cfg, streams=st)):.3f} ms   "
+          f"short-first: {replay_ms(ShortFirst(groups, cfg, streams=st)):.3f} ms")
