@@ -49,6 +49,8 @@ OPS_PER_EDGE = 19  # ALU ops per edge-update per codeword (referenc
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--device-list", default="",
+                    help="explicit CUDA devices for the one-process multi-device path (testing: '0,0')")
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -304,10 +306,15 @@ def run_ours(args):
     # and the max over ranks (CPU tensors), the decode never communicates.
     # Otherwise one process drives N devices: per-device plans, buffers and
     # streams, no process group and no NCCL (north_star subsystem 5).
-    try:
-        devices = resolve_devices(args.gpus, torch.cuda.device_count(), world, local)
-    except ValueError as e:
-        raise SystemExit(str(e))
+    if args.device_list:
+        # code-path check of the multi-device loop on a smaller box (e.g.
+        # "0,0": two arms on one GPU); the line then says which devices ran
+        devices = [int(d) for d in args.device_list.split(",")]
+    else:
+        try:
+            devices = resolve_devices(args.gpus, torch.cuda.device_count(), world, local)
+        except ValueError as e:
+            raise SystemExit(str(e))
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo")
@@ -449,7 +456,7 @@ def run_ours(args):
                                   ": batch shard per GPU, no collective, no NCCL",
                    "overlap": f"{a0.n_ov} streams per device: consecutive independent batches alternate, so one "
                               f"batch's partial last wave shares the SMs with the next batch's first"},
-        "per_device_ms": per_dev_ms,
+        "per_device_ms": per_dev_ms, "devices": devices,
         "p50_batch_latency_ms": float(np.median(step_ms)),
         "p99_batch_latency_ms": float(np.percentile(step_ms, 99)),
         "bler": bler, "success_rate": success, "quality": quality,
