@@ -274,9 +274,10 @@ bool ftm_layout(const nrldpc_plan* p, Shape& sh, MsgLayout& ml) {
     const int w = b.row_start[r + 1] - b.row_start[r];
     const int kind = p->schedule == 1 ? ftm_kind<1>(w) : ftm_kind<2>(w);
     if (kind == 0) {
+      // workspace rows: slots padded to whole uint4 quads ([quad][z][4])
       if (!leading) return false;
-      ml.mb[r] = (uint32_t)b.row_start[r];
-      e_glob = b.row_start[r + 1];
+      ml.mb[r] = (uint32_t)e_glob;
+      e_glob += (w + 3) & ~3;
     } else {
       leading = false;
       if (kind == 1) {
@@ -1110,8 +1111,16 @@ int nrldpc_plan_create(int device, int k_b, int z, int rows_used, const int32_t*
       // layer units with messages addressed by edge index ([edge][z]
       // workspace), or by their on-chip slots
       MsgLayout ml{};
-      if (!ftm_layout(p, p->main, ml))
-        for (int r = 0; r < p->rows; ++r) ml.mb[r] = (uint32_t)p->base.row_start[r];
+      if (!ftm_layout(p, p->main, ml)) {
+        // every row in the workspace, [quad][z][4] with rows padded to
+        // whole quads (FRow kind 0); e_reg = padded slots per group
+        int slots = 0;
+        for (int r = 0; r < p->rows; ++r) {
+          ml.mb[r] = (uint32_t)slots;
+          slots += (p->base.row_start[r + 1] - p->base.row_start[r] + 3) & ~3;
+        }
+        p->main.kp.e_reg = slots;
+      }
       build_units(p, 0, ml, p->main.kp);
     }
     if (precision == NRLDPC_F32) {

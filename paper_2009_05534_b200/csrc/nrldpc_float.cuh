@@ -143,18 +143,29 @@ __device__ __forceinline__ void flt_two_smallest(const uint32_t (&a)[W], uint32_
 template <int PREC, int W, int KIND = 0>
 struct FRow {
   using F = FOps<PREC>;
-  uint32_t off[W], t[W], neg[W], msg[W];
-  uint32_t m1, m2, S, b1, b2;
-  uint32_t* Me;  // global kind: this row's first edge, edge j at Me[j * Z]
+  uint32_t off[W], t[W], neg[W], msg[W], a[W];
+  uint32_t m1, m2, S, beta;
+  uint4* Me;     // global kind: this row's first quad, edges 4q..4q+3 at Me[q * Z]
   uint32_t Ma;   // shared kind: shared address of the row's first message; tensor kind: TMEM address
   // e0: the row's first edge (global kind), byte offset in this thread's
   // shared message row (shared kind) or column in its TMEM slot (tensor kind)
+  static constexpr int NQ = (W + 3) / 4;
   __device__ __forceinline__ void pro(const KParams& p, uint32_t tq, uint32_t e0, uint32_t zl, uint32_t ZL,
-                                      uint32_t* Mg, bool active, uint32_t Ms = 0, uint32_t tbase = 0) {
+                                      uint4* Mg, bool active, uint32_t Ms = 0, uint32_t tbase = 0) {
     uint32_t tsh[W], tcb[W];
     load_row_tables<W>(p, tq, W, tsh, tcb);
     if constexpr (KIND == 0) {
-      Me = Mg + (long long)e0 * p.z;
+      // quad-interleaved workspace: one coalesced 16-byte load per four
+      // edges (e0: the row's first slot, a multiple of 4)
+      Me = Mg + (long long)(e0 >> 2) * p.z;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const uint4 v = active ? Me[(long long)q * p.z] : make_uint4(0u, 0u, 0u, 0u);
+        const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (4 * q + k < W) msg[4 * q + k] = vv[k];
+      }
     } else if constexpr (KIND == 1) {
       Ma = Ms + e0;
     } else {
@@ -164,43 +175,72 @@ struct FRow {
 #pragma unroll
     for (int j = 0; j < W; ++j) {
       off[j] = edge_offset(tsh[j], tcb[j], zl, ZL);
-      if constexpr (KIND == 0) msg[j] = active ? Me[(long long)j * p.z] : 0u;
       if constexpr (KIND == 1) msg[j] = lds_u32(Ma + 4u * j);
     }
   }
-  __device__ __forceinline__ void main(const uint8_t* Lg, uint32_t beta) {
+  __device__ __forceinline__ void main(const uint8_t* Lg, uint32_t beta_) {
     if constexpr (KIND == 2) tm_wait_ld<W>(msg);
     S = 0;
-    uint32_t a[W];
+    beta = beta_;
 #pragma unroll
     for (int j = 0; j < W; ++j) {
       const uint32_t lv = *reinterpret_cast<const uint32_t*>(Lg + off[j]);
-      t[j] = F::sub_clamp(lv, msg[j]);             // decoder.py:300
-      a[j] = F::absv(t[j]);
-      neg[j] = F::neg_mask(t[j]);                  // lvc < 0 (-0 is not negative)
+      if constexpr (PREC == NRLDPC_F16) {
+        // lvc = clip(lv - msg, +-65504) (decoder.py:300, 231): the clipped
+        // magnitude is min(|d|, 65504) (one HMNMX2 with the |.| modifier;
+        // the clip only maps +-inf), the sign is d's. No posterior is -0
+        // (the prologue loads -0 as +0), so d is never -0 and lvc < 0 is
+        // its sign bit.
+        const uint32_t d = h2u(__hsub2(u2h(lv), u2h(msg[j])));
+        a[j] = h2u(__hmin2(__habs2(u2h(d)), u2h(F::sat())));
+        t[j] = (d & F::sign) | a[j];
+        neg[j] = t[j];  // sign bits only are read
+      } else {
+        t[j] = F::sub_clamp(lv, msg[j]);             // decoder.py:300
+        a[j] = F::absv(t[j]);
+        neg[j] = F::neg_mask(t[j]);                  // lvc < 0 (-0 is not negative)
+      }
       S ^= neg[j];
     }
     // the two smallest |t| (kernels.py:247-250 fold from the saturation
     // identity) as a pairwise tree: the same values as the sequential fold
     // (ties give m1 == m2 either way), ~log2(W) deep instead of ~2W
     flt_two_smallest<F, W>(a, m1, m2);
-    b1 = F::mul(beta, m1);                         // dtype(beta) * m
-    b2 = F::mul(beta, m2);
   }
   __device__ __forceinline__ void scatter(uint8_t* Lg, const KParams& p, bool active) {
+    const uint32_t x12 = m1 ^ m2;
+    // f16: the row sign S folded into beta, so dtype(beta) * other carries
+    // it and the edge's own sign is one XOR; a zero magnitude keeps the
+    // sign the reference gives -0 (np.where(sign, -b, b))
+    const uint32_t beta_s = PREC == NRLDPC_F16 ? beta ^ (S & F::sign) : beta;
 #pragma unroll
     for (int j = 0; j < W; ++j) {
-      const uint32_t eq = F::eq_mask(F::absv(t[j]), m1);        // the argmin edge (ties: m1 == m2)
-      const uint32_t mag = (eq & b2) | (~eq & b1);
-      const uint32_t out = mag ^ ((S ^ neg[j]) & F::sign);       // -mag flips the sign bit
-      if constexpr (KIND == 2) msg[j] = out;
+      // the reference's magnitude b = dtype(beta) * (j == argmin ? m2 : m1)
+      // (decoder.py:306-316). Every edge but the argmin has |t| >= m2, the
+      // argmin has |t| = m1 <= m2, so min(|t|, m2) is m1 there and m2
+      // elsewhere, and (m1 ^ m2) ^ min(|t|, m2) selects the other one
+      // bitwise (non-negative values; a tie has m1 == m2 either way). The
+      // multiply runs per edge on the otherwise idle FMA pipe instead of a
+      // compare + select on the busy ALU pipe.
+      const uint32_t other = x12 ^ F::minv(a[j], m2);
+      const uint32_t out = PREC == NRLDPC_F16 ? F::mul(beta_s, other) ^ (neg[j] & F::sign)
+                                              : F::mul(beta, other) ^ ((S ^ neg[j]) & F::sign);  // -mag flips the sign bit
+      if constexpr (KIND == 2 || KIND == 0) msg[j] = out;
       if (active) {
-        if constexpr (KIND == 0) Me[(long long)j * p.z] = out;
         if constexpr (KIND == 1) sts_u32(Ma + 4u * j, out);
         *reinterpret_cast<uint32_t*>(Lg + off[j]) = F::add_clamp(t[j], out);  // decoder.py:318
       }
     }
     if constexpr (KIND == 2) tm_st_row<W>(Ma, msg);  // warp-collective: every thread of an FTM CTA is active
+    if constexpr (KIND == 0) {
+      if (active) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+          Me[(long long)q * p.z] = make_uint4(msg[4 * q], 4 * q + 1 < W ? msg[4 * q + 1] : 0u,
+                                              4 * q + 2 < W ? msg[4 * q + 2] : 0u,
+                                              4 * q + 3 < W ? msg[4 * q + 3] : 0u);
+      }
+    }
   }
 };
 
@@ -289,8 +329,10 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
   const uint32_t zl = (uint32_t)z * 4u;
   const long long n_c = (long long)p.n_blocks * p.z;
   uint8_t* Lg = smem + data_off + (uint32_t)g * p.l_bytes;
-  // edge e at Mg[e * Z]; FTM: only the global rows' e_reg edges have workspace
-  uint32_t* Mg = ws + gg * (long long)(FTM ? p.e_reg : p.n_edges) * p.z + z;
+  // generic schedule: edge e at Mg[e * Z]. Compile-time schedules: e_reg
+  // padded slots per group as [quad][z][4] (FTM: only the global rows)
+  uint32_t* Mg = ws + gg * (long long)p.n_edges * p.z + z;
+  uint4* Mg4 = reinterpret_cast<uint4*>(ws) + gg * (long long)(p.e_reg >> 2) * p.z + z;
   FltState& gs = gstate[g];
   // FTM: shared message rows after L (one group), tensor-memory slot
   const uint32_t Ms = (uint32_t)__cvta_generic_to_shared(Lg + p.l_bytes) + (uint32_t)z * p.m_stride;
@@ -336,21 +378,32 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
         if (lane_valid[0]) v = reinterpret_cast<const uint32_t*>(llr)[cw0 * n_c + n];
       } else {
         const uint16_t* h = reinterpret_cast<const uint16_t*>(llr);
-        const uint32_t lo = lane_valid[0] ? h[cw0 * n_c + n] : 0u;
-        const uint32_t hi = lane_valid[1] ? h[(cw0 + 1) * n_c + n] : 0u;
+        uint32_t lo = lane_valid[0] ? h[cw0 * n_c + n] : 0u;
+        uint32_t hi = lane_valid[1] ? h[(cw0 + 1) * n_c + n] : 0u;
+        // -0 inputs load as +0. The decode never creates a -0 posterior
+        // itself (x - y and x + y are -0 only for a -0 operand, and messages
+        // are subtracted/added to posteriors), so afterwards "lvc < 0" is the
+        // sign bit alone. Every output is unchanged: -0 and +0 compare and
+        // order the same, and only lvc < 0 / |L| reach the results
+        // (decoder.py:300-334).
+        if (lo == 0x8000u) lo = 0u;
+        if (hi == 0x8000u) hi = 0u;
         v = lo | (hi << 16);
       }
       *reinterpret_cast<uint32_t*>(Lg + (uint32_t)n * 4u) = v;
     }
+    if constexpr (BG != 0) {
+      if (active)
+        for (int q = 0; q < (p.e_reg >> 2); ++q) Mg4[(long long)q * p.z] = make_uint4(0u, 0u, 0u, 0u);
+    }
     if constexpr (FTM) {
-      for (int e = 0; e < p.e_reg; ++e) Mg[(long long)e * p.z] = 0u;  // the global rows come first
       uint4* m4 = reinterpret_cast<uint4*>(Lg + p.l_bytes);
       for (uint32_t k = z; k < (p.m_bytes >> 4); k += p.z) m4[k] = make_uint4(0u, 0u, 0u, 0u);
       uint32_t c = 0;
       for (; c + 4 <= p.tm_cols; c += 4) tm_st4(tbase + c, 0u, 0u, 0u, 0u);
       for (; c < p.tm_cols; ++c) tm_st1(tbase + c, 0u);
       tm_wait_st();
-    } else if (active) {
+    } else if (BG == 0 && active) {
       for (int e = 0; e < p.n_edges; ++e) Mg[(long long)e * p.z] = 0u;
     }
   }
@@ -368,14 +421,14 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
       dispatch_unit<BG, 0>(A.x, [&](auto WA, auto WB) {
         constexpr int wa = decltype(WA)::value, wb = decltype(WB)::value;
         FRow<PREC, wa, FTM ? ftm_kind<BG>(wa) : 0> ra;
-        ra.pro(p, A.z, A.w, zl, ZL, Mg, active, Ms, tbase);
+        ra.pro(p, A.z, A.w, zl, ZL, Mg4, active, Ms, tbase);
         if constexpr (wb == 0) {
           if (bar_prev) __syncthreads();
           ra.main(Lg, beta);
           ra.scatter(Lg, p, active);
         } else {
           FRow<PREC, wb, FTM ? ftm_kind<BG>(wb) : 0> rb;
-          rb.pro(p, B.x, B.y, zl, ZL, Mg, active, Ms, tbase);
+          rb.pro(p, B.x, B.y, zl, ZL, Mg4, active, Ms, tbase);
           if (bar_prev) __syncthreads();
           ra.main(Lg, beta);
           rb.main(Lg, beta);

@@ -27,7 +27,9 @@ static cudaError_t launch_float_bg(Shape& sh, int device, const void* llr, long 
   // messages: stream-ordered workspace, [group][edge][z] x 4 bytes (FTM:
   // only the rows kept in global memory)
   uint32_t* ws = nullptr;
-  const size_t ws_bytes = std::max<size_t>(16, (size_t)grid * sh.groups * (FTM ? kp.e_reg : kp.n_edges) * kp.z * 4);
+  // compile-time schedules: e_reg padded slots per group ([quad][z][4]);
+  // generic: n_edges ([edge][z])
+  const size_t ws_bytes = std::max<size_t>(16, (size_t)grid * sh.groups * (BG != 0 ? kp.e_reg : kp.n_edges) * kp.z * 4);
   cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&ws), ws_bytes, device, st);
   if (e != cudaSuccess) return e;
   kern<<<(unsigned)grid, sh.threads, sh.smem, st>>>(kp, llr, ws, o);
