@@ -299,6 +299,11 @@ bool ftm_layout(const nrldpc_plan* p, Shape& sh, MsgLayout& ml) {
   sh.kp.m_bytes = (uint32_t)mb;
   sh.kp.m_stride = e * 4u;
   sh.kp.e_reg = e_glob;
+  // absolute L addressing (one group per CTA): L starts after the CTA state
+  // and one FltState, in the dynamic window after the 1 KB system area
+  // (k_decode_flt checks the address)
+  sh.kp.abs_base = 0x400u + (((uint32_t)kCtaBytes + (uint32_t)sizeof(FltState) + 15u) & ~15u);
+  for (int t = 0; t < NR_MAX_TAB; ++t) sh.kp.cb[t] += sh.kp.abs_base;
   sh.kp.tm_cols = tm_cols;
   sh.kp.tm_slot = slot;
   return true;

@@ -135,12 +135,27 @@ __device__ __forceinline__ void flt_two_smallest(const uint32_t (&a)[W], uint32_
   m2 = F::minv(hi[0], F::sat());
 }
 
+// Posterior access: relative to the group's L array, or (ABSL, the on-chip
+// single-group shapes) at an absolute shared-window address already folded
+// into the graph table's column base, so a gather is LDS [R + UR] with no
+// per-edge address add (as in k_decode_i8's ABS shapes).
+template <bool ABSL>
+__device__ __forceinline__ uint32_t ld_L(const uint8_t* Lg, uint32_t off) {
+  if constexpr (ABSL) return lds_u32(off);
+  else return *reinterpret_cast<const uint32_t*>(Lg + off);
+}
+template <bool ABSL>
+__device__ __forceinline__ void st_L(uint8_t* Lg, uint32_t off, uint32_t v) {
+  if constexpr (ABSL) sts_u32(off, v);
+  else *reinterpret_cast<uint32_t*>(Lg + off) = v;
+}
+
 // One row of a compile-time (BG1/BG2) layer unit in the float engines,
 // split like the int8 RowWork: pro() touches only this thread's own state
 // (graph tables, edge addresses, its messages from the global workspace), so
 // it runs before the barrier that closes the previous layer; main() reads
 // the posteriors.
-template <int PREC, int W, int KIND = 0>
+template <int PREC, int W, int KIND = 0, bool ABSL = false>
 struct FRow {
   using F = FOps<PREC>;
   uint32_t off[W], t[W], neg[W], msg[W], a[W];
@@ -184,7 +199,7 @@ struct FRow {
     beta = beta_;
 #pragma unroll
     for (int j = 0; j < W; ++j) {
-      const uint32_t lv = *reinterpret_cast<const uint32_t*>(Lg + off[j]);
+      const uint32_t lv = ld_L<ABSL>(Lg, off[j]);
       if constexpr (PREC == NRLDPC_F16) {
         // lvc = clip(lv - msg, +-65504) (decoder.py:300, 231): the clipped
         // magnitude is min(|d|, 65504) (one HMNMX2 with the |.| modifier;
@@ -228,7 +243,7 @@ struct FRow {
       if constexpr (KIND == 2 || KIND == 0) msg[j] = out;
       if (active) {
         if constexpr (KIND == 1) sts_u32(Ma + 4u * j, out);
-        *reinterpret_cast<uint32_t*>(Lg + off[j]) = F::add_clamp(t[j], out);  // decoder.py:318
+        st_L<ABSL>(Lg, off[j], F::add_clamp(t[j], out));  // decoder.py:318
       }
     }
     if constexpr (KIND == 2) tm_st_row<W>(Ma, msg);  // warp-collective: every thread of an FTM CTA is active
@@ -246,7 +261,7 @@ struct FRow {
 
 // One row's parity of hard decisions (lvc < 0, -0 not negative) for the
 // end-of-iteration check, with the row weight known at compile time.
-template <int PREC, int W>
+template <int PREC, int W, bool ABSL = false>
 __device__ __forceinline__ void flt_row_parity(const KParams& p, uint32_t tq, const uint8_t* Lg, uint32_t zl,
                                                uint32_t ZL, int (&wc)[2]) {
   using F = FOps<PREC>;
@@ -254,7 +269,7 @@ __device__ __forceinline__ void flt_row_parity(const KParams& p, uint32_t tq, co
   load_row_tables<W>(p, tq, W, tsh, tcb);
   uint32_t par = 0;
 #pragma unroll
-  for (int j = 0; j < W; ++j) par ^= F::neg_mask(*reinterpret_cast<const uint32_t*>(Lg + edge_offset(tsh[j], tcb[j], zl, ZL)));
+  for (int j = 0; j < W; ++j) par ^= F::neg_mask(ld_L<ABSL>(Lg, edge_offset(tsh[j], tcb[j], zl, ZL)));
   if (F::lanes == 1) {
     wc[0] += par >> 31;
   } else {  // half2 masks: lane 0 in bits 0-15, lane 1 in bits 16-31
@@ -265,25 +280,25 @@ __device__ __forceinline__ void flt_row_parity(const KParams& p, uint32_t tq, co
 
 // The full syndrome of a full compile-time graph (rows R..E-1) as
 // straight-line code.
-template <int PREC, int BG, int R = 0, int E = RowW<BG>::n>
+template <int PREC, int BG, bool ABSL, int R = 0, int E = RowW<BG>::n>
 __device__ __forceinline__ void flt_parity_rows(const KParams& p, const uint8_t* Lg, uint32_t zl, uint32_t ZL,
                                                 int (&wc)[2]) {
   if constexpr (R < E) {
-    flt_row_parity<PREC, RowW<BG>::w[R]>(p, row_tq<BG, R>(), Lg, zl, ZL, wc);
-    flt_parity_rows<PREC, BG, R + 1, E>(p, Lg, zl, ZL, wc);
+    flt_row_parity<PREC, RowW<BG>::w[R], ABSL>(p, row_tq<BG, R>(), Lg, zl, ZL, wc);
+    flt_parity_rows<PREC, BG, ABSL, R + 1, E>(p, Lg, zl, ZL, wc);
   }
 }
 
 // Early-stop iterations (see local_check_tm): blocks of STEP straight-line
 // rows; a warp publishes a failing check of a live lane in the group's
 // counters at once, and all warps stop when every live lane has one.
-template <int PREC, int BG, int R, int STEP>
+template <int PREC, int BG, bool ABSL, int R, int STEP>
 __device__ __forceinline__ void flt_parity_rows_early(const KParams& p, const uint8_t* Lg, uint32_t zl, uint32_t ZL,
                                                       int (&wc)[2], bool need_a, bool need_b, bool& pub_a,
                                                       bool& pub_b, int* synd) {
   if constexpr (R < RowW<BG>::n) {
     constexpr int E = R + STEP < RowW<BG>::n ? R + STEP : RowW<BG>::n;
-    flt_parity_rows<PREC, BG, R, E>(p, Lg, zl, ZL, wc);
+    flt_parity_rows<PREC, BG, ABSL, R, E>(p, Lg, zl, ZL, wc);
     const bool leader = (threadIdx.x & 31) == 0;
     if (!pub_a && __any_sync(0xFFFFFFFFu, wc[0] != 0)) {
       if (leader) atomicAdd(&synd[0], 1);
@@ -295,7 +310,7 @@ __device__ __forceinline__ void flt_parity_rows_early(const KParams& p, const ui
     }
     const volatile int* vs = synd;
     if ((!need_a || vs[0] != 0) && (!need_b || vs[1] != 0)) return;
-    flt_parity_rows_early<PREC, BG, E, STEP>(p, Lg, zl, ZL, wc, need_a, need_b, pub_a, pub_b, synd);
+    flt_parity_rows_early<PREC, BG, ABSL, E, STEP>(p, Lg, zl, ZL, wc, need_a, need_b, pub_a, pub_b, synd);
   }
 }
 
@@ -336,6 +351,8 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
   FltState& gs = gstate[g];
   // FTM: shared message rows after L (one group), tensor-memory slot
   const uint32_t Ms = (uint32_t)__cvta_generic_to_shared(Lg + p.l_bytes) + (uint32_t)z * p.m_stride;
+  // FTM: the host folded L's shared-window address into the column bases
+  if (FTM && (uint32_t)__cvta_generic_to_shared(Lg) != p.abs_base) __trap();
   uint32_t tbase = 0;
   if constexpr (FTM) {
     if (tid < 32) {
@@ -414,26 +431,30 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
    if constexpr (BG != 0) {
     // host-built layer units (KParams::unit_a/b, edge indices for messages)
     bool bar_prev = false;
+    // an on-chip (FTM) CTA is one group of exactly blockDim threads and the
+    // grid never holds a CTA without a codeword, so every thread is active:
+    // known at compile time, the message loads and stores need no branch
+    const bool act = FTM ? true : active;
 #pragma unroll 1
     for (int u = 0; u < p.n_units; ++u) {
       const uint4 A = p.unit_a[u];
       const uint4 B = p.unit_b[u];
       dispatch_unit<BG, 0>(A.x, [&](auto WA, auto WB) {
         constexpr int wa = decltype(WA)::value, wb = decltype(WB)::value;
-        FRow<PREC, wa, FTM ? ftm_kind<BG>(wa) : 0> ra;
-        ra.pro(p, A.z, A.w, zl, ZL, Mg4, active, Ms, tbase);
+        FRow<PREC, wa, FTM ? ftm_kind<BG>(wa) : 0, FTM> ra;
+        ra.pro(p, A.z, A.w, zl, ZL, Mg4, act, Ms, tbase);
         if constexpr (wb == 0) {
           if (bar_prev) __syncthreads();
           ra.main(Lg, beta);
-          ra.scatter(Lg, p, active);
+          ra.scatter(Lg, p, act);
         } else {
-          FRow<PREC, wb, FTM ? ftm_kind<BG>(wb) : 0> rb;
-          rb.pro(p, B.x, B.y, zl, ZL, Mg4, active, Ms, tbase);
+          FRow<PREC, wb, FTM ? ftm_kind<BG>(wb) : 0, FTM> rb;
+          rb.pro(p, B.x, B.y, zl, ZL, Mg4, act, Ms, tbase);
           if (bar_prev) __syncthreads();
           ra.main(Lg, beta);
           rb.main(Lg, beta);
-          ra.scatter(Lg, p, active);
-          rb.scatter(Lg, p, active);
+          ra.scatter(Lg, p, act);
+          rb.scatter(Lg, p, act);
         }
       });
       bar_prev = A.y != 0;
@@ -493,11 +514,11 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
         if (p.rows == RowW<BG>::n) {
           if (early) {
             bool pub_a = !need_a, pub_b = !need_b;
-            flt_parity_rows_early<PREC, BG, 0, 4>(p, Lg, zl, ZL, wc, need_a, need_b, pub_a, pub_b, gs.synd);
+            flt_parity_rows_early<PREC, BG, FTM, 0, 4>(p, Lg, zl, ZL, wc, need_a, need_b, pub_a, pub_b, gs.synd);
             wc[0] = wc[1] = 0;  // already counted in gs.synd
             coop = true;
           } else {
-            flt_parity_rows<PREC, BG>(p, Lg, zl, ZL, wc);
+            flt_parity_rows<PREC, BG, FTM>(p, Lg, zl, ZL, wc);
           }
           straight = true;
         }
@@ -509,7 +530,7 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
         uint32_t par = 0;
 #pragma unroll
         for (int j = 0; j < 19; ++j)
-          if (j < w) par ^= F::neg_mask(*reinterpret_cast<const uint32_t*>(Lg + edge_offset(tsh[j], tcb[j], zl, ZL)));
+          if (j < w) par ^= F::neg_mask(ld_L<FTM>(Lg, edge_offset(tsh[j], tcb[j], zl, ZL)));
         if (LANES == 1) {
           wc[0] += par >> 31;
         } else {  // half2 masks: lane 0 in bits 0-15, lane 1 in bits 16-31
