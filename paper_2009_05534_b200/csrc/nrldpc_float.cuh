@@ -131,8 +131,15 @@ __device__ __forceinline__ void flt_two_smallest(const uint32_t (&a)[W], uint32_
     hi[P - 1] = F::sat();
   }
   flt_merge<F, P>(lo, hi);
-  m1 = F::minv(lo[0], F::sat());
-  m2 = F::minv(hi[0], F::sat());
+  if constexpr (F::lanes == 2) {
+    // f16: every |t| is already clipped to 65504 = sat (FRow::main), so the
+    // cap at the fold identity is a no-op
+    m1 = lo[0];
+    m2 = hi[0];
+  } else {
+    m1 = F::minv(lo[0], F::sat());
+    m2 = F::minv(hi[0], F::sat());
+  }
 }
 
 // Posterior access: relative to the group's L array, or (ABSL, the on-chip
@@ -340,7 +347,11 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
   const long long gg = (long long)blockIdx.x * p.groups + g;  // global group index
   const long long cw0 = gg * LANES;
   const bool active = st_ok && cw0 < p.batch;
-  const uint32_t ZL = (uint32_t)p.z * 4u;
+  // ZL through an opaque move: otherwise the compiler rewrites edge_offset's
+  // (zl + s) - ZL as (z - Z) * 4 + s, one more instruction per edge than the
+  // fused add-min (VIADDMNMX) it emits for the int8 kernels
+  uint32_t ZL;
+  asm("mov.b32 %0, %1;" : "=r"(ZL) : "r"((uint32_t)p.z * 4u));
   const uint32_t zl = (uint32_t)z * 4u;
   const long long n_c = (long long)p.n_blocks * p.z;
   uint8_t* Lg = smem + data_off + (uint32_t)g * p.l_bytes;
@@ -435,11 +446,16 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
     // grid never holds a CTA without a codeword, so every thread is active:
     // known at compile time, the message loads and stores need no branch
     const bool act = FTM ? true : active;
+    // the dispatch code is loaded one unit ahead (as in one_iteration), so
+    // the dispatch branch does not wait on the constant load
+    uint32_t ncode = p.unit_a[0].x;
 #pragma unroll 1
     for (int u = 0; u < p.n_units; ++u) {
+      const uint32_t code = ncode;
       const uint4 A = p.unit_a[u];
       const uint4 B = p.unit_b[u];
-      dispatch_unit<BG, 0>(A.x, [&](auto WA, auto WB) {
+      ncode = p.unit_a[u + 1].x;
+      dispatch_unit<BG, 0>(code, [&](auto WA, auto WB) {
         constexpr int wa = decltype(WA)::value, wb = decltype(WB)::value;
         FRow<PREC, wa, FTM ? ftm_kind<BG>(wa) : 0, FTM> ra;
         ra.pro(p, A.z, A.w, zl, ZL, Mg4, act, Ms, tbase);
