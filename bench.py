@@ -308,9 +308,11 @@ def run_ours(args):
     # Otherwise one process drives N devices: per-device plans, buffers and
     # streams, no process group and no NCCL (north_star subsystem 5).
     if args.device_list:
-        # code-path check of the multi-device loop on a smaller box (e.g.
-        # "0,0": two arms on one GPU); the line then says which devices ran
-        devices = [int(d) for d in args.device_list.split(",")]
+        # code-path check of the multi-device paths on a smaller box (e.g.
+        # "0,0": two arms, or two torchrun ranks, on one GPU); the line then
+        # says which devices ran
+        listed = [int(d) for d in args.device_list.split(",")]
+        devices = [listed[local % len(listed)]] if world > 1 else listed
     else:
         try:
             devices = resolve_devices(args.gpus, torch.cuda.device_count(), world, local)
