@@ -22,6 +22,26 @@ struct GroupState {
   int accept[2];
 };
 
+// Add a thread's unsatisfied-check count and min |L| into its group's
+// counters. When warps never straddle groups (Z % 32 == 0) the warp reduces
+// first (REDUX) and one lane issues the shared-memory atomic: 32x fewer
+// atomics on the same two addresses, which otherwise serialise (up to 768
+// per check at 384 threads). on: this thread contributes (padding threads
+// and idle lanes pass false). Every thread of the warp must call it.
+__device__ __forceinline__ void group_accumulate(int* synd, int* minabs, int wc, int ma, bool on, bool whole_warps) {
+  if (whole_warps) {
+    const int s = __reduce_add_sync(0xFFFFFFFFu, on ? wc : 0);
+    const int m = __reduce_min_sync(0xFFFFFFFFu, on ? ma : 255);
+    if ((threadIdx.x & 31) == 0) {
+      if (s) atomicAdd(synd, s);
+      if (m < 255) atomicMin(minabs, m);
+    }
+  } else if (on) {
+    if (wc) atomicAdd(synd, wc);
+    atomicMin(minabs, ma);
+  }
+}
+
 struct CtaState {
   int n_done;
   int n_valid;
@@ -1344,13 +1364,10 @@ __device__ __forceinline__ void decode_i8_cta(const KParams& p, const int8_t* __
       else
         local_check<BG, MAXW, LANES, ABS>(p, zl, ZL, Lg, wc, ma, early, lane_valid[0] && !gs.done[0],
                                           lane_valid[1] && !gs.done[1], gs.synd);
-      if (active) {
+      // minabs starts at 255 and |L| <= 127, so 255 never needs storing
 #pragma unroll
-        for (int l = 0; l < LANES; ++l) {
-          if (wc[l]) atomicAdd(&gs.synd[l], wc[l]);
-          atomicMin(&gs.minabs[l], ma[l]);
-        }
-      }
+      for (int l = 0; l < LANES; ++l)
+        group_accumulate(&gs.synd[l], &gs.minabs[l], wc[l], ma[l], active, p.z % 32 == 0);
     }
     __syncthreads();
     if constexpr (TM) {
@@ -1360,8 +1377,8 @@ __device__ __forceinline__ void decode_i8_cta(const KParams& p, const int8_t* __
                     (lane_valid[1] && !gs.done[1] && gs.synd[1] == 0))) {
         int ma[2];
         margin_tm(p, zl, ZL, p.abs_base, ma);
-        atomicMin(&gs.minabs[0], ma[0]);
-        atomicMin(&gs.minabs[1], ma[1]);
+        group_accumulate(&gs.synd[0], &gs.minabs[0], 0, ma[0], true, true);
+        group_accumulate(&gs.synd[1], &gs.minabs[1], 0, ma[1], true, true);
         __syncthreads();
       }
     }
@@ -1661,10 +1678,7 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const 
       if constexpr (TM) local_check_tm<BG>(p, zl, ZL, p.abs_base, wc, ma, !last[0] && !last[1], act[0], act[1], gs.synd);
       else local_check<BG, MAXW, LANES, ABS>(p, zl, ZL, Lg, wc, ma, !last[0] && !last[1], act[0], act[1], gs.synd);
 #pragma unroll
-      for (int l = 0; l < 2; ++l) {
-        if (wc[l]) atomicAdd(&gs.synd[l], wc[l]);
-        atomicMin(&gs.minabs[l], ma[l]);
-      }
+      for (int l = 0; l < 2; ++l) group_accumulate(&gs.synd[l], &gs.minabs[l], wc[l], ma[l], true, true);
     }
     __syncthreads();
     if constexpr (TM) {
@@ -1672,8 +1686,8 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const 
       if (!last[0] && !last[1] && ((act[0] && gs.synd[0] == 0) || (act[1] && gs.synd[1] == 0))) {
         int ma[2];
         margin_tm(p, zl, ZL, p.abs_base, ma);
-        atomicMin(&gs.minabs[0], ma[0]);
-        atomicMin(&gs.minabs[1], ma[1]);
+        group_accumulate(&gs.synd[0], &gs.minabs[0], 0, ma[0], true, true);
+        group_accumulate(&gs.synd[1], &gs.minabs[1], 0, ma[1], true, true);
         __syncthreads();
       }
     }

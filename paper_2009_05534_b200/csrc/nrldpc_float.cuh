@@ -565,8 +565,20 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
       }
 #pragma unroll
       for (int l = 0; l < LANES; ++l) {
-        if (wc[l]) atomicAdd(&gs.synd[l], wc[l]);
-        atomicMin(reinterpret_cast<int*>(&gs.minabs[l]), __float_as_int(ma[l]));  // non-negative floats
+        // non-negative floats order as their bit patterns; with whole warps
+        // per group (Z % 32 == 0, group-uniform `active`) the warp reduces
+        // first and one lane issues the atomics (see group_accumulate)
+        if (p.z % 32 == 0) {
+          const int s = __reduce_add_sync(0xFFFFFFFFu, wc[l]);
+          const int m = __reduce_min_sync(0xFFFFFFFFu, __float_as_int(ma[l]));
+          if ((threadIdx.x & 31) == 0) {
+            if (s) atomicAdd(&gs.synd[l], s);
+            atomicMin(reinterpret_cast<int*>(&gs.minabs[l]), m);
+          }
+        } else {
+          if (wc[l]) atomicAdd(&gs.synd[l], wc[l]);
+          atomicMin(reinterpret_cast<int*>(&gs.minabs[l]), __float_as_int(ma[l]));
+        }
       }
     }
     __syncthreads();
