@@ -291,13 +291,15 @@ struct RowWork {
   half2 dd, b2s;  // (b1 - b2)' and b2'
   __device__ __forceinline__ void beta_arith(const Consts& k) {
     // floor(beta*m) == RN(beta_h*(m - delta) + C) - C for every m in [0,127]
-    // (verified exhaustively on the host); all FMA-pipe, no table lookups
-    const half2 sig = u2h((S & 0x80008000u) | k.one);
+    // (verified exhaustively on the host); no table lookups
     const half2 bh = u2h(k.bh), nd = u2h(k.nd), cc = u2h(k.cc);
     const half2 B1 = __hfma2(__hadd2(m1, nd), bh, cc);
     const half2 B2 = __hfma2(__hadd2(m2, nd), bh, cc);
-    dd = __hmul2(__hsub2(B1, B2), sig);
-    b2s = __hmul2(__hsub2(B2, cc), sig);
+    // times (-1)^S as a sign-bit flip: one LOP3 each instead of forming
+    // +-1.0 and two HMUL2 (exact, including the sign of a zero)
+    const uint32_t sflip = S & 0x80008000u;
+    dd = u2h(h2u(__hsub2(B1, B2)) ^ sflip);
+    b2s = u2h(h2u(__hsub2(B2, cc)) ^ sflip);
   }
   __device__ __forceinline__ void beta_lut(const uint16_t* __restrict__ lut, uint32_t one) {
     const half2 sig = u2h((S & 0x80008000u) | one);
@@ -470,12 +472,14 @@ struct RowWorkTM {
   }
   half2 dd, b2s;
   __device__ __forceinline__ void beta_arith(const Consts& k) {
-    const half2 sig = u2h((S & 0x80008000u) | k.one);
     const half2 bh = u2h(k.bh), nd = u2h(k.nd), cc = u2h(k.cc);
     const half2 B1 = __hfma2(__hadd2(m1, nd), bh, cc);
     const half2 B2 = __hfma2(__hadd2(m2, nd), bh, cc);
-    dd = __hmul2(__hsub2(B1, B2), sig);
-    b2s = __hmul2(__hsub2(B2, cc), sig);
+    // times (-1)^S as a sign-bit flip: one LOP3 each instead of forming
+    // +-1.0 and two HMUL2 (exact, including the sign of a zero)
+    const uint32_t sflip = S & 0x80008000u;
+    dd = u2h(h2u(__hsub2(B1, B2)) ^ sflip);
+    b2s = u2h(h2u(__hsub2(B2, cc)) ^ sflip);
   }
   __device__ __forceinline__ void scatter(uint32_t* mreg, uint32_t one) {
     const half2 H127 = u2h(0x57F057F0u);   // 127.0
