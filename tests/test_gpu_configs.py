@@ -187,3 +187,33 @@ def test_plan_cache_is_bounded_and_releases_plans(cuda_ok, monkeypatch):
     bg = nr.load_basegraph("BG2", 18)
     res = nr.decode(_blocks(bg, 2, (18, 0)), bg, cfg)  # the cache still works
     assert res.bits.shape == (2, 10 * 18)
+
+
+@pytest.mark.parametrize("bg_id,z,rows", [("BG1", 384, 46), ("BG2", 64, 42), ("BG1", 20, 46)])
+def test_float_signed_zeros_and_overflow_vs_oracle(cuda_ok, bg_id, z, rows):
+    """f16/f32 engines on inputs full of -0/+0, huge magnitudes (the f16 clip
+    at +-65504 binds after the subtract and the add) and ties: bit-exact
+    against the oracle (which follows the reference's numpy float16/32 ops).
+    The f16 engine loads -0 as +0 and treats lvc < 0 as the sign bit."""
+    bg = nr.load_basegraph(bg_id, z)
+    params = nr.code_params(bg, z, rows)
+    rng = np.random.default_rng(z * 7 + rows)
+    B = 12
+    x = rng.normal(0.0, 4.0, size=(B, params.n_c))
+    x[:, : 2 * z] = 0.0
+    zero = rng.random(x.shape) < 0.2
+    x[zero] = np.where(rng.random(zero.sum()) < 0.5, -0.0, 0.0)
+    big = rng.random(x.shape) < 0.05
+    x[big] = np.sign(rng.normal(size=big.sum())) * rng.uniform(3e4, 6.5e4, size=big.sum())
+    x[:2] = np.where(x[:2] == 0, -0.0, x[:2])  # two codewords with every zero negative
+    for prec, dt in (("f16", np.float16), ("f32", np.float32)):
+        blocks = x.astype(dt)
+        for stop in ("none", "syndrome"):
+            cfg = nr.DecodeConfig(precision=prec, max_iter=6, early_stop=stop, beta=0.75)
+            ref = oracle.decode(blocks, bg, cfg)
+            got = nr.decode(blocks, bg, cfg)
+            _same(got, ref)
+            tr_ref, tr = [], []
+            oracle.decode(blocks[:3], bg, cfg, tr_ref)
+            nr.decode(blocks[:3], bg, cfg, tr)
+            assert tr == tr_ref
