@@ -42,6 +42,22 @@ __device__ __forceinline__ void group_accumulate(int* synd, int* minabs, int wc,
   }
 }
 
+// Phase stamps (NRLDPC_PHASES builds only, tools/phase_probe.py): per CTA,
+// globaltimer at kernel entry, after the prologue, before the final check,
+// after the results, at exit.
+#ifdef NRLDPC_PHASES
+__device__ unsigned long long nr_phase_stamps[4096 * 8];
+__device__ __forceinline__ void phase_stamp(long long cta, int k) {
+  if (threadIdx.x == 0 && cta < 4096) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    nr_phase_stamps[cta * 8 + k] = t;
+  }
+}
+#else
+__device__ __forceinline__ void phase_stamp(long long, int) {}
+#endif
+
 struct CtaState {
   int n_done;
   int n_valid;
@@ -1185,6 +1201,7 @@ __device__ __forceinline__ void decode_i8_cta(const KParams& p, const int8_t* __
   GroupState* gstate = reinterpret_cast<GroupState*>(smem + kLutBytes + kCtaBytes);
   const uint32_t data_off = data_offset(p.groups);
 
+  phase_stamp(cta_idx, 0);
   const int tid = threadIdx.x;
   // not a padding thread; register-row shapes have one group of Z threads
   // with Z in {288, 320, 352, 384}, a whole number of warps (host-checked)
@@ -1344,6 +1361,7 @@ __device__ __forceinline__ void decode_i8_cta(const KParams& p, const int8_t* __
     if (bad && o.status) atomicOr(o.status, 1);
   }
   __syncthreads();
+  phase_stamp(cta_idx, 1);
 
   const Consts kc{lds_u32(&cta->kc[0]), lds_u32(&cta->kc[1]), lds_u32(&cta->kc[2]), lds_u32(&cta->kc[3]),
                   lds_u32(&cta->kc[4])};
@@ -1356,6 +1374,7 @@ __device__ __forceinline__ void decode_i8_cta(const KParams& p, const int8_t* __
     else one_iteration<BG, MAXW, LANES, NREG, ABS>(p, rc, rm);
     const bool last = it == p.max_iter;
     if (!(p.early_stop != NRLDPC_STOP_NONE || p.trace || last)) continue;
+    if (last) phase_stamp(cta_idx, 2);
 
     // ---- end-of-iteration check (decoder.py:497-536) ----
     // weights are only needed in full when traced or final
@@ -1368,12 +1387,14 @@ __device__ __forceinline__ void decode_i8_cta(const KParams& p, const int8_t* __
       else
         local_check<BG, MAXW, LANES, ABS>(p, zl, ZL, Lg, wc, ma, early, lane_valid[0] && !gs.done[0],
                                           lane_valid[1] && !gs.done[1], gs.synd);
+      if (last) phase_stamp(cta_idx, 5);
       // minabs starts at 255 and |L| <= 127, so 255 never needs storing
 #pragma unroll
       for (int l = 0; l < LANES; ++l)
         group_accumulate(&gs.synd[l], &gs.minabs[l], wc[l], ma[l], active, p.z % 32 == 0);
     }
     __syncthreads();
+    if (last) phase_stamp(cta_idx, 6);
     if constexpr (TM) {
       // second pass: the margin, only when a live lane's syndrome is zero
       // (block-uniform: shared state read after the barrier)
@@ -1416,6 +1437,7 @@ __device__ __forceinline__ void decode_i8_cta(const KParams& p, const int8_t* __
       if (p.z % 32 == 0) {
         // group-uniform condition, whole warps per group: ballots are safe
         if (need[0] || need[1]) write_bits_warp<LANES, ES>(p, Lg, z, need, cw0, o.bits);
+        if (last) phase_stamp(cta_idx, 7);
       } else {
 #pragma unroll
         for (int l = 0; l < LANES; ++l)
@@ -1467,12 +1489,14 @@ __device__ __forceinline__ void decode_i8_cta(const KParams& p, const int8_t* __
     // uniform datapath (graph tables in uniform registers)
     if (__syncthreads_and(!p.trace && cta->n_done >= cta->n_valid)) break;
   }
+  phase_stamp(cta_idx, 3);
   if constexpr (TM) {
     tm_wait_st();
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(lds_u32(&cta->kc[5])));
   }
+  phase_stamp(cta_idx, 4);
 }
 
 // One launch, one shape: CTA blockIdx.x decodes codewords

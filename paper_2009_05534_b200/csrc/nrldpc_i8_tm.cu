@@ -26,3 +26,9 @@ cudaError_t launch_int8_multi_tm(int kernel, Shape* const* sh, int n, const int8
     default: return cudaErrorInvalidValue;
   }
 }
+
+#ifdef NRLDPC_PHASES
+extern "C" int nrldpc_debug_phases(unsigned long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, nr::nr_phase_stamps, sizeof(unsigned long long) * (size_t)n);
+}
+#endif
