@@ -36,13 +36,13 @@ class Group:
 
 class MixedBatchDecoder:
     def __init__(self, groups: list[Group], cfg: DecodeConfig, streams: int = 16, device: int = 0,
-                 grouped: bool = True):
+                 grouped: bool = True, coscheduled: bool = True):
         import torch
 
         self.cfg = cfg
         self.groups = groups
         # plans tuned for sharing SMs with each other's launches
-        self.plans = [get_plan(g.bg, g.rows_used, cfg, device, coscheduled=True) for g in groups]
+        self.plans = [get_plan(g.bg, g.rows_used, cfg, device, coscheduled=coscheduled) for g in groups]
         dev = torch.device("cuda", device)
         dtype = {"int8": torch.int8, "f16": torch.float16, "f32": torch.float32}[cfg.precision.value]
         # static buffers: callers fill .inputs[i] (or pass arrays to decode())

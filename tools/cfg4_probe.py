@@ -60,3 +60,8 @@ class ShortFirst(MixedBatchDecoder):
 for st in (20, 24, 28, 32, 33, 40, 48):
     print(f"grouped LPT streams={st}: {replay_ms(MixedBatchDecoder(groups, cfg, streams=st)):.3f} ms   "
           f"short-first: {replay_ms(ShortFirst(groups, cfg, streams=st)):.3f} ms")
+
+print("-- plans without the co-scheduling hint (ABS / TM variants where they apply)")
+for st in (16, 24, 32):
+    print(f"grouped, coscheduled=False, streams={st}: "
+          f"{replay_ms(MixedBatchDecoder(groups, cfg, streams=st, coscheduled=False)):.3f} ms")
