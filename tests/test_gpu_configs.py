@@ -217,3 +217,27 @@ def test_float_signed_zeros_and_overflow_vs_oracle(cuda_ok, bg_id, z, rows):
             oracle.decode(blocks[:3], bg, cfg, tr_ref)
             nr.decode(blocks[:3], bg, cfg, tr)
             assert tr == tr_ref
+
+
+@pytest.mark.parametrize("stop", ["none", "syndrome"])
+def test_multi_shape_launch_tm_variants_vs_oracle(cuda_ok, stop):
+    """Multi-shape launches of the TM variants (plans without the
+    co-scheduling hint: BG1 Z=288..384 with register rows, BG1 Z=160..256,
+    BG2 Z=256..384), several shapes per launch, against the oracle."""
+    from paper_2009_05534_b200.mixed import Group, MixedBatchDecoder
+    cfg = nr.DecodeConfig(max_iter=8, early_stop=stop)
+    # same Z, different rows_used: same kernel variant and CTA size, so they
+    # share launches
+    shapes = [("BG1", 384, 46), ("BG1", 384, 12), ("BG1", 384, 30), ("BG1", 352, 46), ("BG1", 256, 46),
+              ("BG1", 256, 9), ("BG2", 384, 42), ("BG2", 384, 20), ("BG2", 256, 42)]
+    groups, data = [], []
+    for i, (bg_id, z, rows) in enumerate(shapes):
+        bg = nr.load_basegraph(bg_id, z)
+        _, llr = noisy_llrs(bg, rows, 1.5, 5 + i, seed=(z, rows, 21))
+        groups.append(Group(bg, rows, 5 + i))
+        data.append(oracle.quantize_i8(llr, z))
+    mixed = MixedBatchDecoder(groups, cfg, streams=4, coscheduled=False)
+    assert any(len(lg) > 1 for lg in mixed.launches)
+    for rep in range(2):
+        for g, res, blocks in zip(groups, mixed.decode(data), data):
+            _same(res, oracle.decode(blocks, g.bg, cfg))
