@@ -218,9 +218,12 @@ struct FRow {
         t[j] = (d & F::sign) | a[j];
         neg[j] = t[j];  // sign bits only are read
       } else {
-        t[j] = F::sub_clamp(lv, msg[j]);             // decoder.py:300
+        // f32 has no clip (decoder.py:300); with no -0 posterior (the
+        // prologue loads -0 as +0) lvc < 0 is again the sign bit of t for
+        // finite posteriors
+        t[j] = F::sub_clamp(lv, msg[j]);
         a[j] = F::absv(t[j]);
-        neg[j] = F::neg_mask(t[j]);                  // lvc < 0 (-0 is not negative)
+        neg[j] = t[j];  // sign bits only are read
       }
       S ^= neg[j];
     }
@@ -231,10 +234,10 @@ struct FRow {
   }
   __device__ __forceinline__ void scatter(uint8_t* Lg, const KParams& p, bool active) {
     const uint32_t x12 = m1 ^ m2;
-    // f16: the row sign S folded into beta, so dtype(beta) * other carries
+    // the row sign S folded into beta, so dtype(beta) * other carries
     // it and the edge's own sign is one XOR; a zero magnitude keeps the
     // sign the reference gives -0 (np.where(sign, -b, b))
-    const uint32_t beta_s = PREC == NRLDPC_F16 ? beta ^ (S & F::sign) : beta;
+    const uint32_t beta_s = beta ^ (S & F::sign);
 #pragma unroll
     for (int j = 0; j < W; ++j) {
       // the reference's magnitude b = dtype(beta) * (j == argmin ? m2 : m1)
@@ -245,8 +248,7 @@ struct FRow {
       // multiply runs per edge on the otherwise idle FMA pipe instead of a
       // compare + select on the busy ALU pipe.
       const uint32_t other = x12 ^ F::minv(a[j], m2);
-      const uint32_t out = PREC == NRLDPC_F16 ? F::mul(beta_s, other) ^ (neg[j] & F::sign)
-                                              : F::mul(beta, other) ^ ((S ^ neg[j]) & F::sign);  // -mag flips the sign bit
+      const uint32_t out = F::mul(beta_s, other) ^ (neg[j] & F::sign);  // -mag flips the sign bit
       if constexpr (KIND == 2 || KIND == 0) msg[j] = out;
       if (active) {
         if constexpr (KIND == 1) sts_u32(Ma + 4u * j, out);
@@ -266,7 +268,7 @@ struct FRow {
   }
 };
 
-// One row's parity of hard decisions (lvc < 0, -0 not negative) for the
+// One row's parity of hard decisions (lvc < 0) for the
 // end-of-iteration check, with the row weight known at compile time.
 template <int PREC, int W, bool ABSL = false>
 __device__ __forceinline__ void flt_row_parity(const KParams& p, uint32_t tq, const uint8_t* Lg, uint32_t zl,
@@ -276,7 +278,9 @@ __device__ __forceinline__ void flt_row_parity(const KParams& p, uint32_t tq, co
   load_row_tables<W>(p, tq, W, tsh, tcb);
   uint32_t par = 0;
 #pragma unroll
-  for (int j = 0; j < W; ++j) par ^= F::neg_mask(ld_L<ABSL>(Lg, edge_offset(tsh[j], tcb[j], zl, ZL)));
+  // no posterior is -0 (the prologue loads -0 as +0), so lvc < 0 is the
+  // sign bit and the row parity is the XOR of the raw words' sign bits
+  for (int j = 0; j < W; ++j) par ^= ld_L<ABSL>(Lg, edge_offset(tsh[j], tcb[j], zl, ZL));
   if (F::lanes == 1) {
     wc[0] += par >> 31;
   } else {  // half2 masks: lane 0 in bits 0-15, lane 1 in bits 16-31
@@ -404,6 +408,7 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
       uint32_t v = 0;
       if (PREC == NRLDPC_F32) {
         if (lane_valid[0]) v = reinterpret_cast<const uint32_t*>(llr)[cw0 * n_c + n];
+        if (v == 0x80000000u) v = 0u;  // -0 loads as +0, as for f16 below
       } else {
         const uint16_t* h = reinterpret_cast<const uint16_t*>(llr);
         uint32_t lo = lane_valid[0] ? h[cw0 * n_c + n] : 0u;
