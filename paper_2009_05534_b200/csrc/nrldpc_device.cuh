@@ -46,12 +46,12 @@ __device__ __forceinline__ void group_accumulate(int* synd, int* minabs, int wc,
 // globaltimer at kernel entry, after the prologue, before the final check,
 // after the results, at exit.
 #ifdef NRLDPC_PHASES
-__device__ unsigned long long nr_phase_stamps[4096 * 8];
+__device__ unsigned long long nr_phase_stamps[4096 * 16];
 __device__ __forceinline__ void phase_stamp(long long cta, int k) {
   if (threadIdx.x == 0 && cta < 4096) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    nr_phase_stamps[cta * 8 + k] = t;
+    nr_phase_stamps[cta * 16 + k] = t;
   }
 }
 #else
@@ -880,6 +880,116 @@ __device__ __forceinline__ void margin_tm(const KParams& p, uint32_t zl, uint32_
   mabs[1] = (int)__high2float(m);
 }
 
+// Bit-sliced final check of the TM layout (Z % 32 == 0, one group per CTA).
+// The hard decisions (decoder.py:323-334: L < 0) of every position are
+// packed once into words, one coalesced LDS and two ballots per 32
+// positions, with the margin min |L| (decoder.py:480-483) folded into the
+// same pass. Check (r, z) is the XOR over the row's edges of the hard bit at
+// ((z + s) mod Z) of the edge's column, so the parities of 32 consecutive
+// checks z = 32i..32i+31 are the XOR of one funnel-shifted word pair per
+// edge: about 1/16 of the instructions of the per-check scan
+// (row_parity_tm). W holds {lane a, lane b} per word, word k covering
+// positions 32k..32k+31 (bit t = position 32k + t); it lives in the message
+// area, dead after the last iteration.
+__device__ __forceinline__ void pack_hard_tm(const KParams& p, uint32_t Ls, uint2* W, int* mabs) {
+  constexpr int PB = 8;  // words per warp per batch: their loads are all in flight together
+  const half2 H255 = u2h(0x5BF85BF8u), H1152 = u2h(0x64806480u);
+  const int lid = threadIdx.x & 31, nwarp = p.z >> 5;
+  const int warp = (int)__reduce_max_sync(0xFFFFFFFFu, threadIdx.x >> 5);  // REDUX: a warp-uniform value for ptxas
+  const int total = p.n_blocks * nwarp;  // words per lane (positions / 32)
+  NR_CHECK((uint32_t)total * 8u <= p.m_bytes);
+  half2 acc = H255;
+  for (int k0 = warp; k0 < total; k0 += PB * nwarp) {
+    uint32_t u[PB];
+#pragma unroll
+    for (int i = 0; i < PB; ++i) {
+      const int k = k0 + i * nwarp;
+      // past the end: a biased +127, which moves neither the margin (the
+      // true minimum is <= 127) nor a stored word
+      u[i] = k < total ? lds_u32(Ls + (uint32_t)(k * 32 + lid) * 4u) : 0x64FF64FFu;
+    }
+    uint32_t va = 0, vb = 0;
+#pragma unroll
+    for (int i = 0; i < PB; ++i) {
+      acc = __hmin2(acc, __habs2(__hsub2(u2h(u[i]), H1152)));
+      // the biased half2's low byte has bit 7 clear exactly for v < 0
+      // (lane a: bit 7, lane b: bit 23)
+      const uint32_t a = __ballot_sync(0xFFFFFFFFu, !(u[i] & 0x80u));
+      const uint32_t b = __ballot_sync(0xFFFFFFFFu, !(u[i] & 0x800000u));
+      if (lid == i) {
+        va = a;
+        vb = b;
+      }
+    }
+    const int k = k0 + lid * nwarp;  // lane i stores the batch's word i
+    if (lid < PB && k < total) W[k] = make_uint2(va, vb);
+  }
+  mabs[0] = (int)__low2float(acc);  // exact small integers
+  mabs[1] = (int)__high2float(acc);
+}
+
+// Parities of checks 32i..32i+31 (lane i < Z/32) of one row of compile-time
+// weight W from the packed hard decisions: the row's table loads (uniform,
+// 128-bit) and all its word loads are in flight together.
+template <int MAXW>
+__device__ __forceinline__ void packed_row_parity(const KParams& p, uint32_t tq, const uint2* W, uint32_t lid,
+                                                  uint32_t nw, int& wa, int& wb) {
+  uint32_t tsh[MAXW], tcb[MAXW];
+  load_row_tables<MAXW>(p, tq, MAXW, tsh, tcb);
+  uint32_t xa = 0, xb = 0;
+#pragma unroll
+  for (int j = 0; j < MAXW; ++j) {
+    const uint32_t s = tsh[j] >> 2;                  // TM tables: shift * 4
+    const uint32_t cw = (tcb[j] - p.abs_base) >> 7;  // column * Z * 4 + base -> column * Z / 32
+    uint32_t q = 32u * (lid < nw ? lid : 0u) + s;
+    if (q >= (uint32_t)p.z) q -= (uint32_t)p.z;
+    const uint32_t k = q >> 5, o = q & 31u;
+    const uint32_t k1 = k + 1 == nw ? 0u : k + 1;
+    NR_CHECK((cw + nw) * 8u <= p.m_bytes);
+    const uint2 lo = W[cw + k], hi = W[cw + k1];
+    xa ^= __funnelshift_r(lo.x, hi.x, o);
+    xb ^= __funnelshift_r(lo.y, hi.y, o);
+  }
+  if (lid < nw) {  // the other lanes ran on a copy of lane 0's checks
+    wa += __popc(xa);
+    wb += __popc(xb);
+  }
+}
+
+// Syndrome weights from the packed hard decisions: warp w takes the rows
+// r with r % (Z/32) == w, lane i the checks 32i..32i+31. Every warp walks
+// the row loop with a uniform test, so the row index, the weight dispatch
+// and the table loads stay on the uniform datapath (LDCU, BRA.U): indexed
+// per-thread constant loads of the tables would miss the constant cache.
+template <int BG>
+__device__ __forceinline__ void packed_parity_tm(const KParams& p, const uint2* W, int& wa, int& wb) {
+  const uint32_t lid = threadIdx.x & 31, nw = (uint32_t)p.z >> 5;
+  const int warp = (int)__reduce_max_sync(0xFFFFFFFFu, threadIdx.x >> 5);  // REDUX: warp-uniform
+  wa = wb = 0;
+  int owner = 0;  // r % (Z/32)
+  for (int r = 0; r < p.rows; ++r) {
+    if (owner == warp) {  // warp-uniform: the whole warp runs the row
+      const uint32_t tq = (uint32_t)p.tab_start[r] / 4u;
+      dispatch_w<BG>(p.row_start[r + 1] - p.row_start[r],
+                     [&](auto WW) { packed_row_parity<decltype(WW)::value>(p, tq, W, lid, nw, wa, wb); });
+    }
+    owner = owner + 1 == (int)nw ? 0 : owner + 1;
+  }
+}
+
+// The hard-decision words of the first K positions straight from the packed
+// words (K = k_b * Z, a whole number of words): coalesced stores.
+__device__ __forceinline__ void write_bits_packed(const KParams& p, const uint2* W, int z, const int (&need)[2],
+                                                  long long cw0, uint32_t* __restrict__ bits) {
+  for (int k = z; k < p.words; k += p.z) {
+    const uint2 v = W[k];
+    NR_CHECK(!need[0] || cw0 < p.batch);
+    NR_CHECK(!need[1] || cw0 + 1 < p.batch);
+    if (need[0]) bits[cw0 * p.words + k] = v.x;
+    if (need[1]) bits[(cw0 + 1) * p.words + k] = v.y;
+  }
+}
+
 // Table slot quad of row R in the compile-time schedules (rows padded to 4
 // slots; host: nrldpc_plan_create's table builder).
 template <int BG, int R>
@@ -1379,12 +1489,26 @@ __device__ __forceinline__ void decode_i8_cta(const KParams& p, const int8_t* __
     // ---- end-of-iteration check (decoder.py:497-536) ----
     // weights are only needed in full when traced or final
     const bool early = BG != 0 && !p.trace && !last && p.z % 32 == 0;
+    // TM, final and untraced: the bit-sliced check (pack_hard_tm), whose
+    // words also give the result bits; the message area is dead by now
+    const bool packed = TM && last && !p.trace;
+    uint2* W = reinterpret_cast<uint2*>(Lg + p.l_bytes);
     {
       int wc[2], ma[2];
-      if constexpr (TM)
-        local_check_tm<BG>(p, zl, ZL, p.abs_base, wc, ma, early, lane_valid[0] && !gs.done[0],
-                           lane_valid[1] && !gs.done[1], gs.synd);
-      else
+      if constexpr (TM) {
+        if (packed) {
+          __syncthreads();  // every message store of the last layer has landed before W reuses the area
+          phase_stamp(cta_idx, 8);
+          pack_hard_tm(p, p.abs_base, W, ma);
+          phase_stamp(cta_idx, 9);
+          __syncthreads();
+          phase_stamp(cta_idx, 10);
+          packed_parity_tm<BG>(p, W, wc[0], wc[1]);
+        } else {
+          local_check_tm<BG>(p, zl, ZL, p.abs_base, wc, ma, early, lane_valid[0] && !gs.done[0],
+                             lane_valid[1] && !gs.done[1], gs.synd);
+        }
+      } else
         local_check<BG, MAXW, LANES, ABS>(p, zl, ZL, Lg, wc, ma, early, lane_valid[0] && !gs.done[0],
                                           lane_valid[1] && !gs.done[1], gs.synd);
       if (last) phase_stamp(cta_idx, 5);
@@ -1436,7 +1560,10 @@ __device__ __forceinline__ void decode_i8_cta(const KParams& p, const int8_t* __
       const int need[2] = {cand[0] || fin[0], LANES == 2 && (cand[1] || fin[1])};
       if (p.z % 32 == 0) {
         // group-uniform condition, whole warps per group: ballots are safe
-        if (need[0] || need[1]) write_bits_warp<LANES, ES>(p, Lg, z, need, cw0, o.bits);
+        if (need[0] || need[1]) {
+          if (packed) write_bits_packed(p, W, z, need, cw0, o.bits);
+          else write_bits_warp<LANES, ES>(p, Lg, z, need, cw0, o.bits);
+        }
         if (last) phase_stamp(cta_idx, 7);
       } else {
 #pragma unroll

@@ -10,6 +10,7 @@ host/mixed/flooding entry points.
   decode() does (decoder.py:287-288).
 """
 
+import ctypes
 import gc
 import weakref
 
@@ -241,3 +242,31 @@ def test_multi_shape_launch_tm_variants_vs_oracle(cuda_ok, stop):
     for rep in range(2):
         for g, res, blocks in zip(groups, mixed.decode(data), data):
             _same(res, oracle.decode(blocks, g.bg, cfg))
+
+
+@pytest.mark.parametrize("bg_id,z,rows,batch", [("BG1", 384, 46, 37), ("BG1", 256, 46, 20), ("BG2", 384, 42, 21),
+                                                ("BG1", 320, 12, 9), ("BG2", 320, 42, 8)])
+@pytest.mark.parametrize("stop", ["none", "syndrome", "crc"])
+def test_bit_sliced_final_check_vs_oracle(cuda_ok, bg_id, z, rows, batch, stop):
+    """The TM layout's final check packs the hard decisions into words and
+    computes 32 checks per funnel-shifted word (pack_hard_tm /
+    packed_parity_tm): at low Eb/N0 most codewords end with a nonzero
+    syndrome, so the final weights, success flags and bits are compared
+    against the oracle, on full and partial graphs and odd batches (the last
+    pair has one live lane)."""
+    bg = nr.load_basegraph(bg_id, z)
+    _, llr = noisy_llrs(bg, rows, -1.0, batch, seed=(z, rows, batch))
+    blocks = oracle.quantize_i8(llr, z)
+    blocks[0] = 0  # an all-erasure codeword: zero syndrome, zero margin, not a success
+    cfg = nr.DecodeConfig(max_iter=4, early_stop=stop)
+    from paper_2009_05534_b200 import _native
+    from paper_2009_05534_b200.decoder import get_plan
+    k, t, sm = ctypes.c_int(), ctypes.c_int(), ctypes.c_int64()
+    _native.check(_native.load().nrldpc_plan_kernel(get_plan(bg, rows, cfg).handle, ctypes.byref(k),
+                                                    ctypes.byref(t), ctypes.byref(sm)))
+    assert k.value in (1, 2, 3), f"expected a TM-layout kernel, got variant {k.value}"
+    ref = oracle.decode(blocks, bg, cfg)
+    res = nr.decode(blocks, bg, cfg)
+    _same(res, ref)
+    assert (ref["syndrome_weight"] > 0).sum() >= batch // 2
+    assert not res.success[0] and res.syndrome_weight[0] == 0

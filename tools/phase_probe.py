@@ -27,10 +27,10 @@ for _ in range(3):
 torch.cuda.synchronize()
 lib = _native.load()
 n = B // 2
-buf = (ctypes.c_ulonglong * (n * 8))()
+buf = (ctypes.c_ulonglong * (n * 16))()
 lib.nrldpc_debug_phases.argtypes = [ctypes.c_void_p, ctypes.c_int]
-assert lib.nrldpc_debug_phases(buf, n * 8) == 0
-t8 = np.array(buf, dtype=np.float64).reshape(n, 8) / 1e3  # us
+assert lib.nrldpc_debug_phases(buf, n * 16) == 0
+t8 = np.array(buf, dtype=np.float64).reshape(n, 16) / 1e3  # us
 t = t8[:, :5]
 d = np.diff(t, axis=1)
 names = ["prologue", "10 iterations", "final check + results", "TMEM dealloc/exit"]
@@ -40,3 +40,7 @@ sub = np.stack([t8[:, 5] - t8[:, 2], t8[:, 6] - t8[:, 5], t8[:, 7] - t8[:, 6], t
 for i, nm in enumerate(["  parity + margin scan", "  counters + barrier", "  bit packing", "  result words + barriers"]):
     print(f"{nm:24s} median {np.median(sub[:, i]):8.2f} us")
 print(f"CTA total median {np.median(t[:, 4] - t[:, 0]):.2f} us; first entry to last exit {t[:, 4].max() - t[:, 0].min():.2f} us")
+if t8[:, 8].any():  # bit-sliced final check (pack_hard_tm / packed_parity_tm)
+    for nm, a, b in (("    barrier after the last layer", 2, 8), ("    pack (hard words + margin)", 8, 9),
+                     ("    barrier", 9, 10), ("    packed parity", 10, 5)):
+        print(f"{nm:34s} median {np.median(t8[:, b] - t8[:, a]):8.2f} us")
