@@ -270,3 +270,17 @@ def test_bit_sliced_final_check_vs_oracle(cuda_ok, bg_id, z, rows, batch, stop):
     _same(res, ref)
     assert (ref["syndrome_weight"] > 0).sum() >= batch // 2
     assert not res.success[0] and res.syndrome_weight[0] == 0
+
+
+def test_random_parity_sweep_short():
+    """tools/parity_sweep.py for 20 s with a fixed seed: random graphs, all
+    51 Z, partial graphs, odd batches, every precision and stop mode, each
+    case bit-exact against the oracle."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, str(root / "tools" / "parity_sweep.py"), "20", "7"], capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert " 0 mismatches" in r.stdout
