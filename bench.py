@@ -642,8 +642,9 @@ def e2e_api(bg, a0, args, k):
     return {"value": B * k * steps / dt / 1e9, "unit": "Gbps", "ms_per_step": dt / steps * 1e3,
             "steps": steps, "h2d_bytes_per_step": int(arrs[0].nbytes), "d2h_bytes_per_step": int(B * (4 * a0.plan.words + 10)),
             "result_bytes_per_step": int(res.bits.nbytes),
-            "path": "paper_2009_05534_b200.decode(numpy pageable int8, bg, cfg) -> DecodeResult (bits unpacked "
-                    "to (B, K) bytes); the drop-in the reference's callers reach",
+            "path": "paper_2009_05534_b200.decode(numpy pageable int8, bg, cfg) -> DecodeResult (bits as (B, K) "
+                    "bytes, unpacked chunk by chunk inside nrldpc_decode_host_bytes); the drop-in the reference's "
+                    "callers reach",
             "pinned_input_value": B * k * steps / dt_pin / 1e9,
             "pinned_input_note": "the same call with the input array in pinned memory (hostmem.pinned_empty): "
                                  "no host staging copy",

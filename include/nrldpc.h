@@ -170,6 +170,19 @@ int nrldpc_decode_host(nrldpc_plan* plan, const void* llr_host, int64_t batch,
                        uint8_t* success, uint8_t* crc_ok, int chunks);
 
 /*
+ * nrldpc_decode_host with the hard decisions returned the way the reference's
+ * DecodeResult holds them: bits is a HOST (batch, K) byte array of 0/1
+ * (decoder.py:332-334, K = k_b * Z) instead of packed words. Each chunk's
+ * packed words are copied back as soon as its decode ends and unpacked by
+ * the library's host threads while later chunks still decode, so the
+ * unpacking overlaps the pipeline instead of following it. Replaces the
+ * decode + unpack pair behind ldpclab.decoder.decode (decoder.py:543-566).
+ */
+int nrldpc_decode_host_bytes(nrldpc_plan* plan, const void* llr_host, int64_t batch,
+                             uint8_t* bits, int32_t* iters, int32_t* synd,
+                             uint8_t* success, uint8_t* crc_ok, int chunks);
+
+/*
  * The same call split in two for pipelined serving: _async enqueues the
  * copies and the decode and returns a ticket at once; nrldpc_host_wait
  * blocks until that call's results are in the host buffers (and reports its

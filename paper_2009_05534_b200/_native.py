@@ -34,6 +34,7 @@ EXPORTS = (
     "nrldpc_demap_quantize",
     "nrldpc_decode",
     "nrldpc_decode_host",
+    "nrldpc_decode_host_bytes",
     "nrldpc_decode_host_async",
     "nrldpc_host_wait",
     "nrldpc_decode_flooding",
@@ -90,6 +91,8 @@ def load() -> ctypes.CDLL:
     lib.nrldpc_decode.restype = c_int
     lib.nrldpc_decode_host.argtypes = [c_void_p, c_void_p, c_int64] + [c_void_p] * 5 + [c_int]
     lib.nrldpc_decode_host.restype = c_int
+    lib.nrldpc_decode_host_bytes.argtypes = [c_void_p, c_void_p, c_int64] + [c_void_p] * 5 + [c_int]
+    lib.nrldpc_decode_host_bytes.restype = c_int
     lib.nrldpc_decode_host_async.argtypes = [c_void_p, c_void_p, c_int64] + [c_void_p] * 5 + [c_int, c_void_p]
     lib.nrldpc_decode_host_async.restype = c_int
     lib.nrldpc_host_wait.argtypes = [c_void_p, c_int64]

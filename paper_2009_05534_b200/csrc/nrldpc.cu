@@ -598,9 +598,9 @@ class HostPool {
 
  private:
   HostPool() {
-    int n = (int)std::thread::hardware_concurrency();
-    if (const char* e = std::getenv("NRLDPC_HOST_THREADS")) n = std::atoi(e);
-    n = std::max(1, std::min(n, 8));
+    int n = std::min((int)std::thread::hardware_concurrency(), 8);
+    if (const char* e = std::getenv("NRLDPC_HOST_THREADS")) n = std::min(std::atoi(e), 64);
+    n = std::max(1, n);
     for (int i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
   }
   ~HostPool() {
@@ -700,6 +700,36 @@ static void host_copy(void* dst, const void* src, size_t n, bool streaming = fal
   pool.run(parts, [=](int i) {
     const size_t o = (size_t)i * per;
     if (o < n) copy(static_cast<uint8_t*>(dst) + o, static_cast<const uint8_t*>(src) + o, std::min(per, n - o));
+  });
+}
+
+// Packed hard-decision words -> the reference's (B, K) bytes 0/1, LSB first
+// (decoder.py:332-334), rows split over the host pool.
+static void unpack_rows_parallel(const uint32_t* words, int64_t batch, int64_t words_per_cw, int64_t k,
+                                 uint8_t* out) {
+  // byte b of a packed word -> 8 output bytes 0/1, LSB first
+  static const auto lut = [] {
+    std::vector<uint64_t> t(256);
+    for (int b = 0; b < 256; ++b) {
+      uint64_t v = 0;
+      for (int i = 0; i < 8; ++i) v |= (uint64_t)((b >> i) & 1) << (8 * i);
+      t[b] = v;
+    }
+    return t;
+  }();
+  HostPool& pool = HostPool::get();
+  const int nt = pool.workers() + 1;
+  const int64_t per = std::max<int64_t>(1, (batch + 4 * nt - 1) / (4 * nt));
+  const int parts = (int)((batch + per - 1) / per);
+  pool.run(parts, [&](int part) {
+    const int64_t c0 = part * per, c1 = std::min(batch, c0 + per);
+    for (int64_t c = c0; c < c1; ++c) {
+      const uint8_t* src = reinterpret_cast<const uint8_t*>(words + c * words_per_cw);
+      uint8_t* dst = out + c * k;
+      const int64_t full = k / 8;
+      for (int64_t i = 0; i < full; ++i) std::memcpy(dst + 8 * i, &lut[src[i]], 8);
+      for (int64_t i = full * 8; i < k; ++i) dst[i] = (src[i >> 3] >> (i & 7)) & 1u;
+    }
   });
 }
 
@@ -871,30 +901,7 @@ int nrldpc_unpack_bits(const uint32_t* words, int64_t batch, int64_t words_per_c
   if (batch < 0 || k < 0 || words_per_cw * 32 < k) return fail(NRLDPC_EINVAL, "bad unpack shape");
   if (batch == 0 || k == 0) return NRLDPC_OK;
   if (!words || !out) return fail(NRLDPC_EINVAL, "NULL buffer");
-  // byte b of a packed word -> 8 output bytes 0/1, LSB first
-  static const auto lut = [] {
-    std::vector<uint64_t> t(256);
-    for (int b = 0; b < 256; ++b) {
-      uint64_t v = 0;
-      for (int i = 0; i < 8; ++i) v |= (uint64_t)((b >> i) & 1) << (8 * i);
-      t[b] = v;
-    }
-    return t;
-  }();
-  HostPool& pool = HostPool::get();
-  const int nt = pool.workers() + 1;
-  const int64_t per = std::max<int64_t>(1, (batch + 4 * nt - 1) / (4 * nt));
-  const int parts = (int)((batch + per - 1) / per);
-  pool.run(parts, [&](int part) {
-    const int64_t c0 = part * per, c1 = std::min(batch, c0 + per);
-    for (int64_t c = c0; c < c1; ++c) {
-      const uint8_t* src = reinterpret_cast<const uint8_t*>(words + c * words_per_cw);
-      uint8_t* dst = out + c * k;
-      const int64_t full = k / 8;
-      for (int64_t i = 0; i < full; ++i) std::memcpy(dst + 8 * i, &lut[src[i]], 8);
-      for (int64_t i = full * 8; i < k; ++i) dst[i] = (src[i >> 3] >> (i & 7)) & 1u;
-    }
-  });
+  unpack_rows_parallel(words, batch, words_per_cw, k, out);
   return NRLDPC_OK;
 }
 
@@ -1183,6 +1190,8 @@ int nrldpc_plan_destroy(nrldpc_plan* plan) {
   for (auto& s : plan->streams)
     if (s) cudaStreamDestroy(s);
   for (auto& e : plan->chunk_ev) cudaEventDestroy(e);
+  for (auto& e : plan->word_ev) cudaEventDestroy(e);
+  if (plan->h_words) cudaFreeHost(plan->h_words);
   for (auto& sl : plan->slot) {
     if (sl.done) cudaEventSynchronize(sl.done), cudaEventDestroy(sl.done);
     if (sl.d_buf) cudaFree(sl.d_buf);
@@ -1356,9 +1365,14 @@ int nrldpc_decode(nrldpc_plan* plan, const void* llr, int64_t batch, uint32_t* b
 // Enqueue one host-buffer decode into slot `si` (caller holds host_mu and has
 // retired the slot's previous call). Returns the number of decode launches
 // through *launches.
+// chunk_words (nrldpc_decode_host_bytes): each chunk's packed words come back
+// on its own decode stream right after its kernel, into plan->h_words, with
+// plan->word_ev[chunk] recorded; `bits` is then unused and the chunk
+// geometry is returned in *n_chunks_out / *chunk_out.
 static int host_enqueue(nrldpc_plan* plan, int si, const void* llr_host, int64_t batch, uint32_t* bits,
                         int32_t* iters, int32_t* synd, uint8_t* success, uint8_t* crc_ok, int chunks,
-                        int* launches_out) {
+                        int* launches_out, bool chunk_words = false, int* n_chunks_out = nullptr,
+                        int64_t* chunk_out = nullptr) {
   auto& sl = plan->slot[si];
   const size_t esz = plan->precision == NRLDPC_INT8 ? 1 : (plan->precision == NRLDPC_F16 ? 2 : 4);
   const size_t n_c = (size_t)plan->n_blocks * plan->z;
@@ -1403,6 +1417,20 @@ static int host_enqueue(nrldpc_plan* plan, int si, const void* llr_host, int64_t
     NR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     plan->chunk_ev.push_back(e);
   }
+  if (chunk_words) {
+    while ((int)plan->word_ev.size() < n_chunks) {
+      cudaEvent_t e;
+      NR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      plan->word_ev.push_back(e);
+    }
+    if (batch * words * 4 > plan->h_words_cap) {
+      uint8_t* hw = reinterpret_cast<uint8_t*>(plan->h_words);
+      NR_CUDA(grow_pinned(hw, plan->h_words_cap, batch * words * 4));
+      plan->h_words = reinterpret_cast<uint32_t*>(hw);
+    }
+    *n_chunks_out = n_chunks;
+    *chunk_out = chunk;
+  }
   int launches = 0;
   // a pageable input is staged through pinned memory chunk by chunk: the
   // host copy of chunk i+1 overlaps the DMA of chunk i (a pageable source
@@ -1432,6 +1460,11 @@ static int host_enqueue(nrldpc_plan* plan, int si, const void* llr_host, int64_t
     const int rc = decode_impl(plan, d_llr + b0 * per_cw_in, nb, o, st);
     if (rc != NRLDPC_OK) return rc;
     launches += g_launches;
+    if (chunk_words) {
+      NR_CUDA(cudaMemcpyAsync(plan->h_words + b0 * words, d_bits + b0 * words, nb * words * 4,
+                              cudaMemcpyDeviceToHost, st));
+      NR_CUDA(cudaEventRecord(plan->word_ev[idx], st));
+    }
   }
   for (int c = 0; c < n_comp; ++c) {
     NR_CUDA(cudaEventRecord(plan->chunk_ev[n_chunks + c], plan->streams[2 + c]));
@@ -1444,7 +1477,7 @@ static int host_enqueue(nrldpc_plan* plan, int si, const void* llr_host, int64_t
     void* host;
     const void* dev;
     size_t n;
-  } outs[5] = {{bits, d_bits, (size_t)batch * words * 4}, {iters, d_iters, (size_t)batch * 4},
+  } outs[5] = {{bits, d_bits, chunk_words ? 0 : (size_t)batch * words * 4}, {iters, d_iters, (size_t)batch * 4},
                {synd, d_synd, (size_t)batch * 4}, {success, d_succ, (size_t)batch},
                {crc_ok, d_crc, crc_ok ? (size_t)batch : 0}};
   sl.n_dst = 0;
@@ -1538,6 +1571,36 @@ int nrldpc_decode_host(nrldpc_plan* plan, const void* llr_host, int64_t batch, u
     cudaEventDestroy(t0);
     cudaEventDestroy(t1);
   }
+  g_launches = launches;
+  return rc;
+}
+
+int nrldpc_decode_host_bytes(nrldpc_plan* plan, const void* llr_host, int64_t batch, uint8_t* bits,
+                             int32_t* iters, int32_t* synd, uint8_t* success, uint8_t* crc_ok, int chunks) {
+  g_launches = 0;
+  int rc = host_check_args(plan, batch, llr_host, bits, iters, synd, success, crc_ok);
+  if (rc != NRLDPC_OK || batch == 0) return rc;
+  std::lock_guard<std::mutex> lock(plan->host_mu);
+  NR_CUDA(cudaSetDevice(plan->device));
+  for (int i = 0; i < nrldpc_plan::kSlots; ++i) {
+    rc = host_retire(plan, i, false);
+    if (rc != NRLDPC_OK) return rc;
+  }
+  int launches = 0, n_chunks = 0;
+  int64_t chunk = 0;
+  rc = host_enqueue(plan, 0, llr_host, batch, nullptr, iters, synd, success, crc_ok, chunks, &launches, true,
+                    &n_chunks, &chunk);
+  if (rc != NRLDPC_OK) return rc;
+  plan->slot[0].ticket = plan->next_ticket++;
+  // unpack each chunk's words as soon as they land, while later chunks
+  // still decode: only the last chunk's unpack is exposed
+  const int64_t words = plan->base.words, k = (int64_t)plan->k_b * plan->z;
+  for (int idx = 0; idx < n_chunks; ++idx) {
+    const int64_t b0 = idx * chunk, nb = std::min<int64_t>(chunk, batch - b0);
+    NR_CUDA(cudaEventSynchronize(plan->word_ev[idx]));
+    unpack_rows_parallel(plan->h_words + b0 * words, nb, words, k, bits + b0 * k);
+  }
+  rc = host_retire(plan, 0, true);
   g_launches = launches;
   return rc;
 }

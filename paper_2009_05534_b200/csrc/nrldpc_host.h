@@ -84,6 +84,9 @@ struct nrldpc_plan {
   static constexpr int kSlots = 2;
   cudaStream_t streams[kHostStreams] = {};
   std::vector<cudaEvent_t> chunk_ev;
+  std::vector<cudaEvent_t> word_ev;  // nrldpc_decode_host_bytes: a chunk's packed words are on the host
+  uint32_t* h_words = nullptr;       // pinned landing area of those words
+  size_t h_words_cap = 0;
   struct Slot {
     void* d_buf = nullptr;
     size_t d_cap = 0;

@@ -244,6 +244,20 @@ class Plan:
             int(chunks)))
         return out
 
+    def decode_host_bytes(self, llr: np.ndarray, chunks: int = 4) -> dict:
+        """decode_host with the hard decisions as the reference's (B, K) bytes
+        (nrldpc_decode_host_bytes): each chunk's words are unpacked by the
+        library's host threads while later chunks still decode."""
+        batch = int(llr.shape[0])
+        llr = np.ascontiguousarray(llr)
+        out = {"bits": np.empty((batch, self.k), np.uint8), "iters": np.empty(batch, np.int32),
+               "synd": np.empty(batch, np.int32), "success": np.empty(batch, np.uint8),
+               "crc_ok": np.empty(batch, np.uint8)}
+        _native.check(_native.load().nrldpc_decode_host_bytes(
+            self.handle, llr.ctypes.data, batch, out["bits"].ctypes.data, out["iters"].ctypes.data,
+            out["synd"].ctypes.data, out["success"].ctypes.data, out["crc_ok"].ctypes.data, int(chunks)))
+        return out
+
 
 # Plans cached per (graph, Z, rows_used, config, device), least recently used
 # first out. An evicted plan is destroyed (nrldpc_plan_destroy: its streams,
@@ -343,10 +357,11 @@ def decode(llrs, bg, cfg: DecodeConfig, trace: list | None = None) -> DecodeResu
         if batch == 0:
             return _empty_result(plan.k, cfg)
         # pageable arrays are staged through the plan's pinned buffers by the
-        # library's host threads, overlapped with the chunks' DMA
-        out = plan.decode_host(host, chunks=max(1, min(12, batch // 86)))
+        # library's host threads, overlapped with the chunks' DMA; the bits
+        # come back as (B, K) bytes, unpacked chunk by chunk in the pipeline
+        out = plan.decode_host_bytes(host, chunks=max(1, min(12, batch // 86)))
         return DecodeResult(
-            bits=unpack_bits(out["bits"], plan.k),
+            bits=out["bits"],
             iterations=out["iters"].astype(np.int64),
             success=out["success"].astype(bool),
             syndrome_weight=out["synd"].astype(np.int64),
