@@ -284,3 +284,23 @@ def test_random_parity_sweep_short():
                        text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert " 0 mismatches" in r.stdout
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_decode_numpy_multi_chunk_bytes_vs_oracle(cuda_ok, pinned):
+    """decode(numpy) with enough codewords for a multi-chunk host pipeline
+    (nrldpc_decode_host_bytes: each chunk's words unpacked into the (B, K)
+    bytes while later chunks decode), from a pageable and a pinned array,
+    bit-exact against the oracle; an odd batch leaves a short last chunk."""
+    bg = nr.load_basegraph("BG2", 64)
+    blocks = _blocks(bg, 1001, seed=11, ebn0=1.0)
+    if pinned:
+        from paper_2009_05534_b200.hostmem import pinned_empty
+        pin = pinned_empty(blocks.shape, torch.int8, 0).numpy()
+        pin[:] = blocks
+        blocks = pin
+    for stop in ("none", "syndrome"):
+        cfg = nr.DecodeConfig(max_iter=6, early_stop=stop)
+        res = nr.decode(blocks, bg, cfg)
+        assert res.bits.dtype == np.uint8 and res.bits.shape == (1001, bg.k_b * 64)
+        _same(res, oracle.decode(np.asarray(blocks), bg, cfg))
