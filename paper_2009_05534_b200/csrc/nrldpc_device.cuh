@@ -1480,19 +1480,6 @@ __device__ __forceinline__ void decode_i8_cta(const KParams& p, const int8_t* __
   RegMsg<NREG> rm;
   rm.init();
   for (int it = 1; it <= p.max_iter; ++it) {
-    if (it == p.max_iter && p.pf_stride && tid == 0) {
-      // the next wave's CTA on this SM starts when this one ends: pull its
-      // input into L2 now, so its prologue loads hit L2 instead of HBM
-      const long long c0 = (cta_idx + p.pf_stride) * p.groups * LANES;
-      if (c0 < p.batch) {
-        const long long n = min((long long)p.groups * LANES, p.batch - c0) * n_c;  // bytes, multiple of 16
-        const int8_t* src = llr + c0 * n_c;
-        for (long long off = 0; off < n; off += 32768) {
-          const uint32_t len = (uint32_t)min(n - off, 32768LL);
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + off), "r"(len) : "memory");
-        }
-      }
-    }
     if constexpr (TM) one_iteration_tm<BG, NREG>(p, tc, rm);
     else one_iteration<BG, MAXW, LANES, NREG, ABS>(p, rc, rm);
     const bool last = it == p.max_iter;

@@ -46,8 +46,6 @@ struct alignas(16) KParams {
   uint32_t crc_poly;
   int trace;         // nonzero: record per-iteration trace, never exit early
   int vec_load;      // rows are 16-byte aligned: vectorized prologue
-  int pf_stride;     // > 0: in its last iteration a CTA prefetches into L2 the
-                     // input of CTA + pf_stride (the next wave on its SM)
   int words;         // ceil(K/32)
   long long batch;
   uint32_t l_bytes;  // per group: n_blocks*z*LANES rounded up to 16

@@ -31,12 +31,6 @@ static cudaError_t launch_i8(Shape& sh, int device, const int8_t* llr, long long
   kp.vec_load = ((long long)kp.n_blocks * kp.z) % 16 == 0 && ((uintptr_t)llr & 15) == 0;
   const long long per_cta = (long long)sh.groups * LANES;
   const long long grid = (batch + per_cta - 1) / per_cta;
-  // a CTA's successor on its SM is about one wave (resident CTAs) later
-  static int sms[64] = {};
-  if (!sms[device & 63]) cudaDeviceGetAttribute(&sms[device & 63], cudaDevAttrMultiProcessorCount, device);
-  const long long wave = (long long)sh.occ * sms[device & 63];
-  static const bool no_pf = getenv("NRLDPC_NO_PREFETCH") != nullptr;
-  kp.pf_stride = kp.vec_load && grid > wave && !no_pf ? (int)wave : 0;
   kern<<<(unsigned)grid, sh.threads, sh.smem, st>>>(kp, llr, o);
   ++g_launches;
   return cudaGetLastError();
