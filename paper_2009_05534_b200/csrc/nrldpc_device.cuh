@@ -957,10 +957,11 @@ __device__ __forceinline__ void packed_row_parity(const KParams& p, uint32_t tq,
 }
 
 // Syndrome weights from the packed hard decisions: warp w takes the rows
-// r with r % (Z/32) == w, lane i the checks 32i..32i+31. Every warp walks
-// the row loop with a uniform test, so the row index, the weight dispatch
-// and the table loads stay on the uniform datapath (LDCU, BRA.U): indexed
-// per-thread constant loads of the tables would miss the constant cache.
+// r with r % (Z/32) == w, lane i the checks 32i..32i+31 (lanes >= Z/32 run
+// a copy of lane 0's checks and do not count them). The phase is latency-
+// bound (dependent table and word loads per row); a per-thread row loop and
+// tables staged in shared memory measured no faster
+// (profiles/r02_cta_phases.txt).
 template <int BG>
 __device__ __forceinline__ void packed_parity_tm(const KParams& p, const uint2* W, int& wa, int& wb) {
   const uint32_t lid = threadIdx.x & 31, nw = (uint32_t)p.z >> 5;
