@@ -1906,6 +1906,17 @@ __global__ void __launch_bounds__(NREG ? 384 : 512, 1) k_decode_i8_refill(const 
           const uint32_t zb = (TM ? 0x64806480u : 0x80808080u) & ~keep_m;
           if constexpr (TM) {
             uint32_t c = 0;
+            // 16 columns per round trip: four loads in flight, one wait
+            for (; c + 16 <= p.tm_cols; c += 16) {
+              uint32_t r[16];
+#pragma unroll
+              for (int q = 0; q < 16; q += 4) tm_ld4(tbase + c + q, r[q], r[q + 1], r[q + 2], r[q + 3]);
+              tm_wait_ld<16>(r);
+#pragma unroll
+              for (int q = 0; q < 16; q += 4)
+                tm_st4(tbase + c + q, (r[q] & keep_m) | zb, (r[q + 1] & keep_m) | zb, (r[q + 2] & keep_m) | zb,
+                       (r[q + 3] & keep_m) | zb);
+            }
             for (; c + 4 <= p.tm_cols; c += 4) {
               uint32_t r[4];
               tm_ld4(tbase + c, r[0], r[1], r[2], r[3]);
