@@ -303,7 +303,7 @@ __device__ __forceinline__ void flt_parity_rows(const KParams& p, const uint8_t*
 // Early-stop iterations (see local_check_tm): blocks of STEP straight-line
 // rows; a warp publishes a failing check of a live lane in the group's
 // counters at once, and all warps stop when every live lane has one.
-template <int PREC, int BG, bool ABSL, int R, int STEP>
+template <int PREC, int BG, bool ABSL, int R, int STEP, int NEXT = STEP>
 __device__ __forceinline__ void flt_parity_rows_early(const KParams& p, const uint8_t* Lg, uint32_t zl, uint32_t ZL,
                                                       int (&wc)[2], bool need_a, bool need_b, bool& pub_a,
                                                       bool& pub_b, int* synd) {
@@ -321,7 +321,7 @@ __device__ __forceinline__ void flt_parity_rows_early(const KParams& p, const ui
     }
     const volatile int* vs = synd;
     if ((!need_a || vs[0] != 0) && (!need_b || vs[1] != 0)) return;
-    flt_parity_rows_early<PREC, BG, ABSL, E, STEP>(p, Lg, zl, ZL, wc, need_a, need_b, pub_a, pub_b, synd);
+    flt_parity_rows_early<PREC, BG, ABSL, E, NEXT, NEXT>(p, Lg, zl, ZL, wc, need_a, need_b, pub_a, pub_b, synd);
   }
 }
 
@@ -535,7 +535,8 @@ __global__ void __launch_bounds__(512) k_decode_flt(const __grid_constant__ KPar
         if (p.rows == RowW<BG>::n) {
           if (early) {
             bool pub_a = !need_a, pub_b = !need_b;
-            flt_parity_rows_early<PREC, BG, FTM, 0, 4>(p, Lg, zl, ZL, wc, need_a, need_b, pub_a, pub_b, gs.synd);
+            // first block one row, then eight (as the int8 kernels, parity_rows_early_tm)
+            flt_parity_rows_early<PREC, BG, FTM, 0, 1, 8>(p, Lg, zl, ZL, wc, need_a, need_b, pub_a, pub_b, gs.synd);
             wc[0] = wc[1] = 0;  // already counted in gs.synd
             coop = true;
           } else {
