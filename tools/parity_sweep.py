@@ -6,7 +6,8 @@ max_iter, beta) cases for a time budget, decodes each through the public
 `decode` and through the oracle (oracle/, the CPU restatement pinned to the
 reference's golden vectors), and reports every mismatch. A companion to the
 fixed-case GPU tests: it walks the shape space (all 51 Z, partial graphs,
-odd batches) the fixed cases only sample.
+odd batches) the fixed cases only sample. One case in ten is a random mixed
+batch through MixedBatchDecoder (multi-shape launches in a CUDA graph).
 
     python tools/parity_sweep.py [seconds=240] [seed=0]
 """
@@ -41,6 +42,35 @@ def case(rng):
     return bg, rows, batch, cfg, ebn0
 
 
+def mixed_case(rng, seed, n):
+    """A random mixed batch (MixedBatchDecoder: multi-shape launches in one
+    CUDA-graph replay) of 2..12 int8 groups, each group against the oracle."""
+    from paper_2009_05534_b200.mixed import Group, MixedBatchDecoder
+    stop = str(rng.choice(["none", "syndrome", "crc"]))
+    cfg = nr.DecodeConfig(early_stop=stop, max_iter=int(rng.integers(1, 11)))
+    groups, data = [], []
+    for g in range(int(rng.integers(2, 13))):
+        bg = nr.load_basegraph("BG1" if rng.random() < 0.5 else "BG2", int(rng.choice(nr.ALL_LIFTING_SIZES)))
+        if stop == "crc" and bg.k_b * bg.z < 40:
+            bg = nr.load_basegraph(bg.id, 384)
+        rows = int(bg.m_bg if rng.random() < 0.7 else rng.integers(4, bg.m_bg + 1))
+        batch = int(rng.integers(1, 12))
+        _, llr = noisy_llrs(bg, rows, float(rng.uniform(-1.0, 4.0)), batch, seed=(seed, n, g))
+        groups.append(Group(bg, rows, batch))
+        data.append(oracle.quantize_i8(llr, bg.z))
+    mixed = MixedBatchDecoder(groups, cfg, streams=int(rng.integers(1, 9)), grouped=bool(rng.random() < 0.8))
+    ok, cws = True, 0
+    for res, g, blocks in zip(mixed.decode(data), groups, data):
+        ref = oracle.decode(blocks, g.bg, cfg)
+        ok = ok and np.array_equal(res.bits, ref["bits"]) and np.array_equal(res.iterations, ref["iterations"]) \
+            and np.array_equal(res.success, ref["success"]) \
+            and np.array_equal(res.syndrome_weight, ref["syndrome_weight"])
+        cws += g.batch
+    if not ok:
+        print(f"MISMATCH mixed batch {[(g.bg.id, g.bg.z, g.rows_used, g.batch) for g in groups]} {cfg}", flush=True)
+    return ok, cws
+
+
 def main():
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 240.0
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 0
@@ -48,6 +78,12 @@ def main():
     t0 = time.time()
     n = bad = cw = 0
     while time.time() - t0 < budget:
+        if rng.random() < 0.1:  # one case in ten is a mixed batch
+            ok, c = mixed_case(rng, seed, n)
+            bad += 0 if ok else 1
+            n += 1
+            cw += c
+            continue
         bg, rows, batch, cfg, ebn0 = case(rng)
         _, llr = noisy_llrs(bg, rows, ebn0, batch, seed=(seed, n))
         if cfg.precision.value == "int8":
