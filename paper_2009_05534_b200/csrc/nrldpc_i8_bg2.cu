@@ -33,3 +33,10 @@ cudaError_t launch_int8_multi_bg2(int kernel, Shape* const* sh, int n, const int
     default: return cudaErrorInvalidValue;
   }
 }
+
+#ifdef NRLDPC_PHASES
+// the BG2 kernels' own copy of the stamps (each translation unit has one)
+extern "C" int nrldpc_debug_phases_bg2(unsigned long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, nr::nr_phase_stamps, sizeof(unsigned long long) * (size_t)n);
+}
+#endif
