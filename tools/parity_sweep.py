@@ -7,7 +7,8 @@ max_iter, beta) cases for a time budget, decodes each through the public
 reference's golden vectors), and reports every mismatch. A companion to the
 fixed-case GPU tests: it walks the shape space (all 51 Z, partial graphs,
 odd batches) the fixed cases only sample. One case in ten is a random mixed
-batch through MixedBatchDecoder (multi-shape launches in a CUDA graph).
+batch through MixedBatchDecoder (multi-shape launches in a CUDA graph), and
+about one in seven single-shape cases also compares the per-iteration trace.
 
     python tools/parity_sweep.py [seconds=240] [seed=0]
 """
@@ -91,9 +92,11 @@ def main():
         else:
             dt = np.float16 if cfg.precision.value == "f16" else np.float32
             blocks = np.concatenate([np.zeros((batch, 2 * bg.z)), llr], axis=1).astype(dt)
-        ref = oracle.decode(blocks, bg, cfg)
-        got = nr.decode(blocks, bg, cfg)
-        ok = (np.array_equal(got.bits, ref["bits"]) and np.array_equal(got.iterations, ref["iterations"])
+        traced = rng.random() < 0.15  # per-iteration (codeword, iteration, weight, margin) trace
+        tr_ref, tr = ([], []) if traced else (None, None)
+        ref = oracle.decode(blocks, bg, cfg, tr_ref)
+        got = nr.decode(blocks, bg, cfg, tr)
+        ok = (tr == tr_ref and np.array_equal(got.bits, ref["bits"]) and np.array_equal(got.iterations, ref["iterations"])
               and np.array_equal(got.success, ref["success"])
               and np.array_equal(got.syndrome_weight, ref["syndrome_weight"]))
         if cfg.early_stop.value == "crc":
